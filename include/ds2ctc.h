@@ -1,0 +1,139 @@
+/*
+ * ds2ctc.h -- C-ABI of the B200-native Deep Speech 2 CTC loss + gradient.
+ *
+ * Drop-in boundary for the reference's CTC entry point
+ *   asr::ctc::ctc_loss_reference(const Matrix& frame_logits,
+ *                                const std::vector<int>& label, int blank)
+ *   (/root/reference/proj/include/asr/ctc.hpp:84-87, proj/src/ctc.cpp:171-207)
+ * as the trainer drives it, one utterance at a time, inside
+ *   asr::trainer::train_epoch (proj/src/trainer.cpp:155-171)
+ * and, cost-only, inside evaluate_mean_loss (trainer.cpp:201-214).
+ *
+ * The reference has no batched API; this header defines the batched,
+ * warp-ctc-style boundary that SURVEY.md §8b specifies. Its contract is
+ * per-utterance equivalence with ctc_loss_reference on the slice
+ * X[0:T_b, b, :] widened to fp64:
+ *
+ *   costs[b]          = ctc_loss_reference(...).loss           (fp32; +inf if infeasible)
+ *   gradients[t][b][:] = ctc_loss_reference(...).logit_grad(t,:) for t < T_b,
+ *                        0 for T_b <= t < T_max, and all-zero rows for an
+ *                        infeasible utterance (the trainer's convention,
+ *                        trainer.cpp:160-166).
+ *
+ * Tolerance: |cost - ref| / |ref| <= 1e-4 and max |grad - ref| <= 1e-4 (fp32
+ * outputs vs the fp64 reference). The summation order differs from the
+ * reference (linear-space occupancy sums instead of log-space folds,
+ * ctc.cpp:76; log p from the alpha/beta meet point instead of the last alpha
+ * column, ctc.cpp:188) -- see DESIGN.md §Numerics.
+ *
+ * All entry points are thread-safe across distinct (device, stream, workspace).
+ * No exceptions cross the ABI; errors are status codes.
+ */
+#ifndef DS2CTC_H
+#define DS2CTC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DS2CTC_STATUS_SUCCESS = 0,
+  DS2CTC_STATUS_INVALID_VALUE = 1,   /* bad shape/length/label/blank, or workspace too small */
+  DS2CTC_STATUS_EXECUTION_FAILED = 2,/* CUDA launch / runtime error */
+  DS2CTC_STATUS_MEMOPS_FAILED = 3,   /* host<->device copy or allocation failure */
+  DS2CTC_STATUS_UNSUPPORTED = 4      /* e.g. 2L+1 > DS2CTC_MAX_STATES, or no sm_100 device */
+} ds2ctc_status;
+
+/* Largest blank-extended label (2L+1) one utterance may have. */
+#define DS2CTC_MAX_STATES 4095
+
+/* Human-readable status. Replaces the reference's exception messages
+ * ("asr: ...", proj/include/asr/common.hpp:37-44). */
+const char* ds2ctc_status_string(ds2ctc_status status);
+
+/* Library version string ("ds2ctc <semver> sm_100a"). */
+const char* ds2ctc_version(void);
+
+/*
+ * Device workspace needed by ds2ctc_compute_loss for this batch shape.
+ * label_lengths / input_lengths are HOST arrays [minibatch]. alphabet_size
+ * INCLUDES the blank (A = reference alphabet_size + 1, network.cpp:135).
+ * Replaces the reference's per-call Matrix allocations (ctc.cpp:175,181,197,
+ * the KeyGroups of ctc.cpp:195): the caller owns all memory.
+ */
+ds2ctc_status ds2ctc_get_workspace_size(const int* label_lengths, const int* input_lengths, int alphabet_size,
+                                        int minibatch, size_t* bytes);
+
+/*
+ * CTC loss and gradient for a batch.
+ *   activations   DEVICE fp32 [T_max][minibatch][alphabet_size], pre-softmax logits,
+ *                 T_max = max(input_lengths). Softmax is applied internally
+ *                 (ctc.hpp:37-40), so logits and log-probabilities are interchangeable.
+ *   gradients     DEVICE fp32, same shape, or NULL for cost only (evaluate_mean_loss,
+ *                 trainer.cpp:201-214; datapipe.cpp:99). Gradient w.r.t. the
+ *                 pre-softmax activations (ctc.cpp:69-79).
+ *   flat_labels   HOST int32, concatenation of the minibatch labels (sum(label_lengths)).
+ *   label_lengths HOST int32 [minibatch].
+ *   input_lengths HOST int32 [minibatch], each in [0, T_max].
+ *   blank_label   index of the blank in [0, alphabet_size); the trainer uses
+ *                 alphabet_size - 1 (trainer.cpp:127).
+ *   costs         DEVICE fp32 [minibatch] (-log p, +inf when infeasible).
+ *   workspace     DEVICE, at least ds2ctc_get_workspace_size() bytes, 256-byte aligned.
+ *   stream        cudaStream_t (NULL = legacy default stream). Asynchronous.
+ * minibatch == 0 is a valid no-op (an empty data-parallel shard, trainer.cpp:141-155).
+ */
+ds2ctc_status ds2ctc_compute_loss(const float* activations, float* gradients, const int* flat_labels,
+                                  const int* label_lengths, const int* input_lengths, int alphabet_size,
+                                  int minibatch, int blank_label, float* costs, void* workspace, void* stream);
+
+/* Same as ds2ctc_compute_loss, but checks the workspace size explicitly. */
+ds2ctc_status ds2ctc_compute_loss_checked(const float* activations, float* gradients, const int* flat_labels,
+                                          const int* label_lengths, const int* input_lengths, int alphabet_size,
+                                          int minibatch, int blank_label, float* costs, void* workspace,
+                                          size_t workspace_bytes, void* stream);
+
+/*
+ * Host-buffer entry point: the reference-facing call (the reference takes and
+ * returns host matrices). activations / gradients / costs are HOST arrays in
+ * the layout above (pinned memory gives full PCIe bandwidth); the library
+ * copies them through a per-thread device context on `device`, runs the same
+ * kernels, copies the results back and synchronises before returning.
+ */
+ds2ctc_status ds2ctc_compute_loss_host(const float* activations, float* gradients, const int* flat_labels,
+                                       const int* label_lengths, const int* input_lengths, int alphabet_size,
+                                       int minibatch, int blank_label, float* costs, int device);
+
+/* ---------------------------------------------------------------------
+ * H1 host scheduler (trainer.cpp:58-91, 140-143) -- pure host functions.
+ * ------------------------------------------------------------------- */
+
+/* SortaGrad visiting order, identical to asr::trainer::sortagrad_order
+ * (trainer.cpp:58-91): epoch 0 stable-sorts by length; later epochs shuffle
+ * whole minibatches with Rng(seed*0x9e3779b9 + epoch + 1). out_order[n]. */
+ds2ctc_status ds2ctc_sortagrad_order(const int* lengths, int n, int global_batch, int epoch, uint64_t seed,
+                                     int sortagrad_on, int64_t* out_order);
+
+/* The reference's contiguous rank slice of one global minibatch
+ * (trainer.cpp:140-143): [*begin, *end) positions within the batch. */
+ds2ctc_status ds2ctc_rank_slice(int batch_n, int minibatch_size, int rank, int* begin, int* end);
+
+/*
+ * Length-aware re-deal of one global minibatch across `world` GPUs:
+ * longest-processing-time-first on the estimated cost of each utterance,
+ * T_b * (1 + alphabet/1024) (serial chain ~ T_b frames, HBM ~ T_b * alphabet
+ * bytes; ties broken by label length). out_rank[n] receives the rank
+ * of each utterance; ranks keep the batch's SortaGrad composition, and the
+ * per-utterance results are order-independent, so parity is unaffected.
+ * out_load (nullable, [world]) receives each rank's estimated cost.
+ */
+ds2ctc_status ds2ctc_shard_lpt(const int* input_lengths, const int* label_lengths, int n, int alphabet_size,
+                               int world, int* out_rank, double* out_load);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DS2CTC_H */

@@ -1,0 +1,93 @@
+"""ctypes binding of libds2ctc.so (the C-ABI in include/ds2ctc.h).
+
+This is the binding a Python caller of the reference's CTC would add; there
+is no fallback: if the in-tree library is missing or cannot be loaded, every
+call raises (the product never silently runs anything on the CPU).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libds2ctc.so")
+
+STATUS = {
+    0: "SUCCESS",
+    1: "INVALID_VALUE",
+    2: "EXECUTION_FAILED",
+    3: "MEMOPS_FAILED",
+    4: "UNSUPPORTED",
+}
+
+# Every symbol include/ds2ctc.h declares (tests check the .so exports them all).
+EXPORTS = (
+    "ds2ctc_status_string",
+    "ds2ctc_version",
+    "ds2ctc_get_workspace_size",
+    "ds2ctc_compute_loss",
+    "ds2ctc_compute_loss_checked",
+    "ds2ctc_compute_loss_host",
+    "ds2ctc_sortagrad_order",
+    "ds2ctc_rank_slice",
+    "ds2ctc_shard_lpt",
+)
+
+
+class Ds2CtcError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        super().__init__(f"{where}: ds2ctc status {status} ({STATUS.get(status, '?')})")
+
+
+_lock = threading.Lock()
+_lib = None
+
+_p = ctypes.c_void_p
+_ip = ctypes.POINTER(ctypes.c_int)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_dp = ctypes.POINTER(ctypes.c_double)
+_szp = ctypes.POINTER(ctypes.c_size_t)
+
+
+def lib():
+    """Loads the in-tree libds2ctc.so (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_1512_02595_b200.build` "
+                                  "(there is no CPU fallback)")
+            L = ctypes.CDLL(LIB_PATH)
+            L.ds2ctc_status_string.restype = ctypes.c_char_p
+            L.ds2ctc_status_string.argtypes = [ctypes.c_int]
+            L.ds2ctc_version.restype = ctypes.c_char_p
+            L.ds2ctc_version.argtypes = []
+            L.ds2ctc_get_workspace_size.restype = ctypes.c_int
+            L.ds2ctc_get_workspace_size.argtypes = [_ip, _ip, ctypes.c_int, ctypes.c_int, _szp]
+            L.ds2ctc_compute_loss.restype = ctypes.c_int
+            L.ds2ctc_compute_loss.argtypes = [_p, _p, _ip, _ip, _ip, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p, _p,
+                                              _p]
+            L.ds2ctc_compute_loss_checked.restype = ctypes.c_int
+            L.ds2ctc_compute_loss_checked.argtypes = [_p, _p, _ip, _ip, _ip, ctypes.c_int, ctypes.c_int,
+                                                      ctypes.c_int, _p, _p, ctypes.c_size_t, _p]
+            L.ds2ctc_compute_loss_host.restype = ctypes.c_int
+            L.ds2ctc_compute_loss_host.argtypes = [_p, _p, _ip, _ip, _ip, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                   _p, ctypes.c_int]
+            L.ds2ctc_sortagrad_order.restype = ctypes.c_int
+            L.ds2ctc_sortagrad_order.argtypes = [_ip, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_uint64,
+                                                 ctypes.c_int, _i64p]
+            L.ds2ctc_rank_slice.restype = ctypes.c_int
+            L.ds2ctc_rank_slice.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _ip, _ip]
+            L.ds2ctc_shard_lpt.restype = ctypes.c_int
+            L.ds2ctc_shard_lpt.argtypes = [_ip, _ip, ctypes.c_int, ctypes.c_int, ctypes.c_int, _ip, _dp]
+            _lib = L
+    return _lib
+
+
+def check(status: int, where: str) -> None:
+    if status != 0:
+        raise Ds2CtcError(status, where)

@@ -1,0 +1,331 @@
+// ctc_api.cpp -- C-ABI of libds2ctc (include/ds2ctc.h): validation, per-call
+// metadata (the reference's augment_label / min_frames / group_rows_by_key,
+// ctc.cpp:47-66,91-107, done once per utterance on the host), workspace
+// layout, and the kernel pipeline on the caller's stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <numeric>
+#include <utility>
+#include <vector>
+
+#include "ds2ctc.h"
+#include "ds2ctc_internal.h"
+
+namespace ds2ctc {
+namespace {
+
+// Pinned staging ring for the per-call metadata blob, one per (thread, device).
+// A slot is reused only after the event recorded behind its last copy fired.
+class Staging {
+ public:
+  ~Staging() {
+    for (auto& s : slots_) {
+      if (s.ev) cudaEventDestroy(s.ev);
+      if (s.ptr) cudaFreeHost(s.ptr);
+    }
+  }
+  // Returns a pinned buffer of at least `bytes`, or nullptr.
+  void* acquire(size_t bytes, cudaEvent_t* ev_out) {
+    Slot& s = slots_[next_];
+    next_ = (next_ + 1) % kSlots;
+    if (s.ev) cudaEventSynchronize(s.ev);
+    if (s.cap < bytes) {
+      if (s.ptr) cudaFreeHost(s.ptr);
+      s.ptr = nullptr;
+      s.cap = 0;
+      size_t want = std::max<size_t>(bytes, 64 << 10);
+      if (cudaMallocHost(&s.ptr, want) != cudaSuccess) return nullptr;
+      s.cap = want;
+    }
+    if (!s.ev && cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    *ev_out = s.ev;
+    return s.ptr;
+  }
+
+ private:
+  static constexpr int kSlots = 4;
+  struct Slot {
+    void* ptr = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+  };
+  Slot slots_[kSlots];
+  int next_ = 0;
+};
+
+Staging& staging_for_current_device() {
+  thread_local std::map<int, Staging> per_device;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return per_device[dev];
+}
+
+int min_frames(const int* label, int L) {  // ctc.cpp:102-107
+  int needed = L;
+  for (int i = 1; i < L; ++i)
+    if (label[i] == label[i - 1]) ++needed;
+  return needed;
+}
+
+ds2ctc_status validate(const int* label_lengths, const int* input_lengths, int A, int B, int blank,
+                       const int* flat_labels) {
+  if (B < 0 || A < 2 || blank < 0 || blank >= A) return DS2CTC_STATUS_INVALID_VALUE;
+  if (B > 0 && (label_lengths == nullptr || input_lengths == nullptr)) return DS2CTC_STATUS_INVALID_VALUE;
+  long long sum_L = 0;
+  for (int b = 0; b < B; ++b) {
+    if (label_lengths[b] < 0 || input_lengths[b] < 0) return DS2CTC_STATUS_INVALID_VALUE;
+    if (2LL * label_lengths[b] + 1 > kMaxStates) return DS2CTC_STATUS_UNSUPPORTED;
+    sum_L += label_lengths[b];
+  }
+  if (sum_L > 0 && flat_labels == nullptr) return DS2CTC_STATUS_INVALID_VALUE;
+  for (long long i = 0; i < sum_L; ++i)
+    if (flat_labels[i] < 0 || flat_labels[i] >= A) return DS2CTC_STATUS_INVALID_VALUE;
+  return DS2CTC_STATUS_SUCCESS;
+}
+
+// Builds the metadata blob (int32 words laid out per Layout) into `blob`.
+// Returns the max S over utterances that run the lattice.
+int build_metadata(const Layout& lay, const int* flat_labels, const int* label_lengths, const int* input_lengths,
+                   int B, int blank, std::vector<int32_t>& blob) {
+  blob.assign(lay.meta_end / sizeof(int32_t), 0);
+  auto* desc = reinterpret_cast<UttDesc*>(blob.data() + lay.desc / 4);
+  int* order = blob.data() + lay.order / 4;
+  int* labels = blob.data() + lay.labels / 4;
+  int* key_char = blob.data() + lay.key_char / 4;
+  int* key_start = blob.data() + lay.key_start / 4;
+  int* key_rows = blob.data() + lay.key_rows / 4;
+  if (lay.sum_L > 0) std::memcpy(labels, flat_labels, sizeof(int) * lay.sum_L);
+
+  long long lab_off = 0, key_off = 0, store_off = 0, occ_off = 0;
+  int max_S = 1;
+  std::vector<std::pair<int, int>> kv;
+  for (int b = 0; b < B; ++b) {
+    UttDesc& u = desc[b];
+    const int T = input_lengths[b], L = label_lengths[b];
+    const int* lab = flat_labels + lab_off;
+    u.T = T;
+    u.L = L;
+    u.S = 2 * L + 1;
+    u.status = T < min_frames(lab, L) ? 1 : (T == 0 ? 2 : 0);
+    u.lab_off = static_cast<int>(lab_off);
+    u.row_off = static_cast<int>(lab_off);
+    u.key_off = static_cast<int>(key_off);
+    u.store_off = store_off;
+    u.occ_off = occ_off;
+    u.tm = T > 0 ? (T - 1) / 2 : 0;
+    // Key groups (ctc.cpp:47-66): slot 0 = blank (even rows are summed on the
+    // device; only odd rows whose label equals the blank id are listed),
+    // slots 1.. = distinct non-blank symbols ascending, rows ascending.
+    kv.clear();
+    for (int i = 0; i < L; ++i) kv.emplace_back(lab[i] == blank ? -1 : lab[i], 2 * i + 1);
+    std::sort(kv.begin(), kv.end());
+    int nkey = 1;
+    key_char[key_off] = blank;
+    int* ks = key_start + key_off + b;
+    ks[0] = 0;
+    int r = 0;
+    size_t i = 0;
+    while (i < kv.size() && kv[i].first == -1) key_rows[lab_off + r++] = kv[i++].second;
+    ks[1] = r;
+    while (i < kv.size()) {
+      const int sym = kv[i].first;
+      key_char[key_off + nkey] = sym;
+      while (i < kv.size() && kv[i].first == sym) key_rows[lab_off + r++] = kv[i++].second;
+      ks[++nkey] = r;
+    }
+    u.nkey = nkey;
+    if (u.status == 0) max_S = std::max(max_S, u.S);
+    lab_off += L;
+    key_off += L + 1;
+    store_off += static_cast<long long>(u.S) * (T + 1);
+    occ_off += static_cast<long long>(T) * (L + 1);
+  }
+  // Longest first (the serial chain is ~T steps), so long pairs start in the first wave.
+  std::iota(order, order + B, 0);
+  std::stable_sort(order, order + B, [&](int x, int y) {
+    const int tx = desc[x].status == 0 ? desc[x].T : -1;
+    const int ty = desc[y].status == 0 ? desc[y].T : -1;
+    return tx > ty;
+  });
+  return max_S;
+}
+
+ds2ctc_status run(const float* acts, float* grads, const int* flat_labels, const int* label_lengths,
+                  const int* input_lengths, int A, int B, int blank, float* costs, void* workspace,
+                  size_t workspace_bytes, bool check_ws, void* stream) {
+  ds2ctc_status st = validate(label_lengths, input_lengths, A, B, blank, flat_labels);
+  if (st != DS2CTC_STATUS_SUCCESS) return st;
+  if (B == 0) return DS2CTC_STATUS_SUCCESS;
+  const Layout lay = make_layout(label_lengths, input_lengths, A, B);
+  if (costs == nullptr || workspace == nullptr) return DS2CTC_STATUS_INVALID_VALUE;
+  if (lay.t_max > 0 && acts == nullptr) return DS2CTC_STATUS_INVALID_VALUE;
+  if (check_ws && workspace_bytes < lay.total) return DS2CTC_STATUS_INVALID_VALUE;
+  if (reinterpret_cast<uintptr_t>(workspace) % kAlign != 0) return DS2CTC_STATUS_INVALID_VALUE;
+
+  thread_local std::vector<int32_t> blob;
+  const int max_S = build_metadata(lay, flat_labels, label_lengths, input_lengths, B, blank, blob);
+
+  auto* ws = static_cast<unsigned char*>(workspace);
+  auto s = static_cast<cudaStream_t>(stream);
+  cudaEvent_t ev = nullptr;
+  void* pinned = staging_for_current_device().acquire(lay.meta_end, &ev);
+  if (pinned == nullptr) return DS2CTC_STATUS_MEMOPS_FAILED;
+  std::memcpy(pinned, blob.data(), lay.meta_end);
+  if (cudaMemcpyAsync(ws, pinned, lay.meta_end, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return DS2CTC_STATUS_MEMOPS_FAILED;
+  if (cudaEventRecord(ev, s) != cudaSuccess) return DS2CTC_STATUS_MEMOPS_FAILED;
+
+  ChainArgs a{};
+  a.x = acts;
+  a.grad = grads;
+  a.costs = costs;
+  a.desc = reinterpret_cast<const UttDesc*>(ws + lay.desc);
+  a.order = reinterpret_cast<const int*>(ws + lay.order);
+  a.labels = reinterpret_cast<const int*>(ws + lay.labels);
+  a.key_char = reinterpret_cast<const int*>(ws + lay.key_char);
+  a.key_start = reinterpret_cast<const int*>(ws + lay.key_start);
+  a.key_rows = reinterpret_cast<const int*>(ws + lay.key_rows);
+  a.stats = reinterpret_cast<const float2*>(ws + lay.stats);
+  a.store = reinterpret_cast<double*>(ws + lay.store);
+  a.occ = (grads != nullptr && A > kFusedMaxAlphabet) ? reinterpret_cast<float*>(ws + lay.occ) : nullptr;
+  a.logz = reinterpret_cast<double*>(ws + lay.logz);
+  a.t_max = lay.t_max;
+  a.B = B;
+  a.A = A;
+  a.blank = blank;
+  int nt = std::min(1024, (max_S + 31) / 32 * 32);
+  if (grads != nullptr && A <= kFusedMaxAlphabet) nt = std::max(nt, (A + 31) / 32 * 32);
+  a.nthreads = std::max(nt, 32);
+  a.cells = (max_S + a.nthreads - 1) / a.nthreads;
+
+  if (launch_rowstats(a, stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  if (launch_chain(a, stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  if (a.occ != nullptr && launch_dense(a, stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  return DS2CTC_STATUS_SUCCESS;
+}
+
+// Per-thread device context of the host-buffer entry point.
+struct HostContext {
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  void* acts = nullptr;
+  size_t acts_cap = 0;
+  void* grads = nullptr;
+  size_t grads_cap = 0;
+  void* costs = nullptr;
+  size_t costs_cap = 0;
+  void* ws = nullptr;
+  size_t ws_cap = 0;
+  ~HostContext() {
+    if (device < 0) return;
+    cudaSetDevice(device);
+    cudaFree(acts);
+    cudaFree(grads);
+    cudaFree(costs);
+    cudaFree(ws);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+bool grow(void** p, size_t* cap, size_t want) {
+  if (*cap >= want) return true;
+  cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  if (want == 0) return true;
+  if (cudaMalloc(p, want) != cudaSuccess) return false;
+  *cap = want;
+  return true;
+}
+
+}  // namespace
+}  // namespace ds2ctc
+
+using namespace ds2ctc;
+
+extern "C" {
+
+const char* ds2ctc_status_string(ds2ctc_status status) {
+  switch (status) {
+    case DS2CTC_STATUS_SUCCESS: return "no error";
+    case DS2CTC_STATUS_INVALID_VALUE: return "invalid value";
+    case DS2CTC_STATUS_EXECUTION_FAILED: return "execution failed";
+    case DS2CTC_STATUS_MEMOPS_FAILED: return "memory operation failed";
+    case DS2CTC_STATUS_UNSUPPORTED: return "unsupported configuration";
+  }
+  return "unknown status";
+}
+
+const char* ds2ctc_version(void) { return "ds2ctc 0.1.0 sm_100a"; }
+
+ds2ctc_status ds2ctc_get_workspace_size(const int* label_lengths, const int* input_lengths, int alphabet_size,
+                                        int minibatch, size_t* bytes) {
+  if (bytes == nullptr || minibatch < 0 || alphabet_size < 2) return DS2CTC_STATUS_INVALID_VALUE;
+  if (minibatch > 0 && (label_lengths == nullptr || input_lengths == nullptr)) return DS2CTC_STATUS_INVALID_VALUE;
+  for (int b = 0; b < minibatch; ++b) {
+    if (label_lengths[b] < 0 || input_lengths[b] < 0) return DS2CTC_STATUS_INVALID_VALUE;
+    if (2LL * label_lengths[b] + 1 > kMaxStates) return DS2CTC_STATUS_UNSUPPORTED;
+  }
+  *bytes = minibatch == 0 ? 0 : make_layout(label_lengths, input_lengths, alphabet_size, minibatch).total;
+  return DS2CTC_STATUS_SUCCESS;
+}
+
+ds2ctc_status ds2ctc_compute_loss(const float* activations, float* gradients, const int* flat_labels,
+                                  const int* label_lengths, const int* input_lengths, int alphabet_size,
+                                  int minibatch, int blank_label, float* costs, void* workspace, void* stream) {
+  return run(activations, gradients, flat_labels, label_lengths, input_lengths, alphabet_size, minibatch,
+             blank_label, costs, workspace, 0, false, stream);
+}
+
+ds2ctc_status ds2ctc_compute_loss_checked(const float* activations, float* gradients, const int* flat_labels,
+                                          const int* label_lengths, const int* input_lengths, int alphabet_size,
+                                          int minibatch, int blank_label, float* costs, void* workspace,
+                                          size_t workspace_bytes, void* stream) {
+  return run(activations, gradients, flat_labels, label_lengths, input_lengths, alphabet_size, minibatch,
+             blank_label, costs, workspace, workspace_bytes, true, stream);
+}
+
+ds2ctc_status ds2ctc_compute_loss_host(const float* activations, float* gradients, const int* flat_labels,
+                                       const int* label_lengths, const int* input_lengths, int alphabet_size,
+                                       int minibatch, int blank_label, float* costs, int device) {
+  ds2ctc_status st = validate(label_lengths, input_lengths, alphabet_size, minibatch, blank_label, flat_labels);
+  if (st != DS2CTC_STATUS_SUCCESS) return st;
+  if (minibatch == 0) return DS2CTC_STATUS_SUCCESS;
+  if (costs == nullptr) return DS2CTC_STATUS_INVALID_VALUE;
+  thread_local std::map<int, HostContext> contexts;
+  if (cudaSetDevice(device) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  HostContext& ctx = contexts[device];
+  if (ctx.device < 0) {
+    ctx.device = device;
+    if (cudaStreamCreateWithFlags(&ctx.stream, cudaStreamNonBlocking) != cudaSuccess)
+      return DS2CTC_STATUS_EXECUTION_FAILED;
+  }
+  const Layout lay = make_layout(label_lengths, input_lengths, alphabet_size, minibatch);
+  const size_t elems = static_cast<size_t>(lay.t_max) * minibatch * alphabet_size;
+  if (elems > 0 && activations == nullptr) return DS2CTC_STATUS_INVALID_VALUE;
+  if (!grow(&ctx.acts, &ctx.acts_cap, elems * sizeof(float)) ||
+      !grow(&ctx.grads, &ctx.grads_cap, gradients ? elems * sizeof(float) : 0) ||
+      !grow(&ctx.costs, &ctx.costs_cap, minibatch * sizeof(float)) || !grow(&ctx.ws, &ctx.ws_cap, lay.total))
+    return DS2CTC_STATUS_MEMOPS_FAILED;
+  if (elems > 0 &&
+      cudaMemcpyAsync(ctx.acts, activations, elems * sizeof(float), cudaMemcpyHostToDevice, ctx.stream) != cudaSuccess)
+    return DS2CTC_STATUS_MEMOPS_FAILED;
+  st = run(static_cast<const float*>(ctx.acts), gradients ? static_cast<float*>(ctx.grads) : nullptr, flat_labels,
+           label_lengths, input_lengths, alphabet_size, minibatch, blank_label, static_cast<float*>(ctx.costs), ctx.ws,
+           ctx.ws_cap, true, ctx.stream);
+  if (st != DS2CTC_STATUS_SUCCESS) return st;
+  if (gradients && elems > 0 &&
+      cudaMemcpyAsync(gradients, ctx.grads, elems * sizeof(float), cudaMemcpyDeviceToHost, ctx.stream) != cudaSuccess)
+    return DS2CTC_STATUS_MEMOPS_FAILED;
+  if (cudaMemcpyAsync(costs, ctx.costs, minibatch * sizeof(float), cudaMemcpyDeviceToHost, ctx.stream) != cudaSuccess)
+    return DS2CTC_STATUS_MEMOPS_FAILED;
+  if (cudaStreamSynchronize(ctx.stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  return DS2CTC_STATUS_SUCCESS;
+}
+
+}  // extern "C"

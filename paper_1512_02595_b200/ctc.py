@@ -1,0 +1,152 @@
+"""Host-side mirror of the reference CTC interface, over the C-ABI.
+
+Reference interface (proj/include/asr/ctc.hpp:62-87):
+
+    struct CtcResult { bool feasible; real loss; Matrix logit_grad; };
+    CtcResult ctc_loss_reference(const Matrix& frame_logits,
+                                 const std::vector<int>& label, int blank);
+
+``ctc_loss`` keeps that signature and meaning (one utterance, T x A logits,
+blank passed explicitly, loss = -log p, gradient w.r.t. pre-softmax logits,
+infeasible -> feasible=False, loss=+inf, empty gradient), computed on the
+B200 through ``ds2ctc_compute_loss_host``. ``compute_ctc_loss`` is the
+batched device entry point the trainer loop (trainer.cpp:155-171) maps onto:
+``[T_max][B][A]`` fp32 CUDA activations in, per-utterance costs and
+``[T_max][B][A]`` gradients out, all on the caller's CUDA stream.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+
+_ip = ctypes.POINTER(ctypes.c_int)
+
+
+@dataclass
+class CtcResult:
+    """asr::ctc::CtcResult (ctc.hpp:62-66)."""
+
+    feasible: bool
+    loss: float
+    logit_grad: np.ndarray  # T x A; empty (0 x 0) when infeasible
+
+
+def _i32(a) -> np.ndarray:
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.int32).reshape(-1))
+    return arr if arr.size else np.zeros(1, dtype=np.int32)
+
+
+def _iptr(a: np.ndarray):
+    return a.ctypes.data_as(_ip)
+
+
+def workspace_size(label_lengths, input_lengths, alphabet_size: int) -> int:
+    """ds2ctc_get_workspace_size: device bytes needed for one call."""
+    ll = _i32(label_lengths)
+    il = _i32(input_lengths)
+    B = int(np.asarray(label_lengths).size)
+    out = ctypes.c_size_t()
+    _lib.check(_lib.lib().ds2ctc_get_workspace_size(_iptr(ll), _iptr(il), alphabet_size, B, ctypes.byref(out)),
+               "ds2ctc_get_workspace_size")
+    return int(out.value)
+
+
+class Workspace:
+    """Grow-only device workspace (a torch uint8 buffer, 256-byte aligned)."""
+
+    def __init__(self, device=None):
+        self.device = device
+        self.buf = None
+
+    def get(self, nbytes: int):
+        import torch
+
+        if self.buf is None or self.buf.numel() < nbytes + 256:
+            self.buf = torch.empty(max(nbytes + 256, 1 << 20), dtype=torch.uint8, device=self.device)
+        ptr = self.buf.data_ptr()
+        return (ptr + 255) // 256 * 256, self.buf.numel() - ((ptr + 255) // 256 * 256 - ptr)
+
+
+_default_ws = {}
+
+
+def compute_ctc_loss(activations, flat_labels, label_lengths, input_lengths, blank: Optional[int] = None,
+                     want_grad: bool = True, gradients=None, costs=None, workspace: Optional[Workspace] = None,
+                     stream=None):
+    """Batched CTC on the GPU via ds2ctc_compute_loss_checked.
+
+    activations: torch.float32 CUDA tensor [T_max, B, A] (time-major, contiguous),
+    T_max == max(input_lengths). flat_labels / label_lengths / input_lengths are host
+    int sequences. Returns (costs [B] fp32 CUDA, gradients [T_max, B, A] or None).
+    Asynchronous on `stream` (default: torch's current stream).
+    """
+    import torch
+
+    if not (activations.is_cuda and activations.dtype == torch.float32 and activations.is_contiguous()):
+        raise ValueError("activations must be a contiguous float32 CUDA tensor [T, B, A]")
+    T_max, B, A = activations.shape
+    ll = _i32(label_lengths)
+    il = _i32(input_lengths)
+    labels = _i32(flat_labels)
+    if int(np.asarray(input_lengths).size) != B or int(np.asarray(label_lengths).size) != B:
+        raise ValueError("label_lengths / input_lengths must have B entries")
+    if B and int(np.max(np.asarray(input_lengths))) != T_max:
+        raise ValueError("activations.shape[0] must equal max(input_lengths)")
+    blank = A - 1 if blank is None else int(blank)
+    dev = activations.device
+    if costs is None:
+        costs = torch.empty(B, dtype=torch.float32, device=dev)
+    if want_grad and gradients is None:
+        gradients = torch.empty_like(activations)
+    if not want_grad:
+        gradients = None
+    if workspace is None:
+        workspace = _default_ws.setdefault(dev.index, Workspace(dev))
+    need = workspace_size(label_lengths, input_lengths, A)
+    ws_ptr, ws_bytes = workspace.get(need)
+    if stream is None:
+        stream = torch.cuda.current_stream(dev)
+    st = _lib.lib().ds2ctc_compute_loss_checked(
+        ctypes.c_void_p(activations.data_ptr()),
+        ctypes.c_void_p(gradients.data_ptr()) if gradients is not None else None,
+        _iptr(labels), _iptr(ll), _iptr(il), A, B, blank, ctypes.c_void_p(costs.data_ptr()),
+        ctypes.c_void_p(ws_ptr), ws_bytes, ctypes.c_void_p(stream.cuda_stream))
+    _lib.check(st, "ds2ctc_compute_loss")
+    return costs, gradients
+
+
+def compute_ctc_loss_host(activations: np.ndarray, flat_labels, label_lengths, input_lengths,
+                          blank: Optional[int] = None, want_grad: bool = True, device: int = 0,
+                          gradients: Optional[np.ndarray] = None, costs: Optional[np.ndarray] = None):
+    """Host buffers in, host buffers out (ds2ctc_compute_loss_host); synchronous."""
+    acts = np.ascontiguousarray(activations, dtype=np.float32)
+    T_max, B, A = acts.shape
+    blank = A - 1 if blank is None else int(blank)
+    if costs is None:
+        costs = np.empty(max(B, 1), dtype=np.float32)
+    if want_grad and gradients is None:
+        gradients = np.empty_like(acts)
+    st = _lib.lib().ds2ctc_compute_loss_host(
+        ctypes.c_void_p(acts.ctypes.data),
+        ctypes.c_void_p(gradients.ctypes.data) if want_grad else None,
+        _iptr(_i32(flat_labels)), _iptr(_i32(label_lengths)), _iptr(_i32(input_lengths)), A, B, blank,
+        ctypes.c_void_p(costs.ctypes.data), device)
+    _lib.check(st, "ds2ctc_compute_loss_host")
+    return costs[:B], (gradients if want_grad else None)
+
+
+def ctc_loss(frame_logits, label: Sequence[int], blank: int, device: int = 0) -> CtcResult:
+    """Drop-in for asr::ctc::ctc_loss_reference (ctc.cpp:171-207) on one utterance."""
+    x = np.ascontiguousarray(np.asarray(frame_logits, dtype=np.float32))
+    T, A = x.shape
+    lab = list(int(c) for c in label)
+    costs, grads = compute_ctc_loss_host(x.reshape(T, 1, A), lab, [len(lab)], [T], blank=blank, device=device)
+    loss = float(costs[0])
+    if not np.isfinite(loss):
+        return CtcResult(False, float("inf"), np.zeros((0, 0), dtype=np.float32))
+    return CtcResult(True, loss, grads.reshape(T, A))

@@ -1,0 +1,65 @@
+"""Data-parallel CTC step over torch.distributed (NCCL on B200, gloo in CPU tests).
+
+The reference's only cross-worker interaction on the CTC path is the ring
+all-reduce of the two scalars {local_loss, local_skipped}
+(proj/src/trainer.cpp:174-180, allreduce.cpp:301-341). Here each rank
+computes its shard of the global minibatch (H1: SortaGrad composition, LPT
+deal) and the scalars cross NVLink in ONE tiny collective. For run-to-run
+determinism like the reference ring's fixed fold order (allreduce.hpp:91-95),
+the per-rank pairs are all-gathered and folded in rank order on every rank.
+Empty shards still join the collective (trainer.cpp:141-155,173-180).
+"""
+from __future__ import annotations
+
+from typing import Callable, Tuple
+
+import numpy as np
+
+from . import scheduler
+
+
+def reduce_loss_skipped(local_loss: float, local_skipped: int, device=None) -> Tuple[float, int]:
+    """Rank-order-deterministic sum of {loss, skipped} over the default process group."""
+    import torch
+    import torch.distributed as dist
+
+    pair = torch.tensor([float(local_loss), float(local_skipped)], dtype=torch.float64, device=device)
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(pair[0]), int(pair[1])
+    world = dist.get_world_size()
+    out = torch.empty(world * 2, dtype=torch.float64, device=device)
+    dist.all_gather_into_tensor(out, pair)
+    vals = out.view(world, 2).cpu().numpy()
+    loss = 0.0
+    skipped = 0.0
+    for r in range(world):  # fixed rank order, like the ring's fold (allreduce.cpp:326)
+        loss = loss + vals[r, 0]
+        skipped = skipped + vals[r, 1]
+    return float(loss), int(skipped)
+
+
+def local_loss_skipped(costs: np.ndarray) -> Tuple[float, int]:
+    """trainer.cpp:160-168: infeasible utterances are skipped, the rest summed (in order)."""
+    loss = 0.0
+    skipped = 0
+    for c in np.asarray(costs, dtype=np.float64):
+        if np.isfinite(c):
+            loss += float(c)
+        else:
+            skipped += 1
+    return loss, skipped
+
+
+def dp_ctc_step(batch_input_lengths, batch_label_lengths, alphabet_size: int, rank: int, world: int,
+                compute: Callable[[np.ndarray], np.ndarray], device=None):
+    """One data-parallel CTC step for a global minibatch.
+
+    compute(indices) must return this rank's per-utterance costs for the
+    given minibatch indices (the GPU path in bench.py; any function in tests).
+    Returns (global loss sum, global skipped count, this rank's indices).
+    """
+    idx = scheduler.shard_batch(batch_input_lengths, batch_label_lengths, alphabet_size, world, rank)
+    costs = compute(idx) if idx.size else np.zeros(0)
+    loss, skipped = local_loss_skipped(costs)
+    g_loss, g_skipped = reduce_loss_skipped(loss, skipped, device=device)
+    return g_loss, g_skipped, idx

@@ -1,0 +1,106 @@
+"""C-ABI checks that need no GPU: the in-tree library loads, exports every
+symbol include/ds2ctc.h declares, sizes workspaces, and rejects bad input
+with the documented status codes before touching CUDA."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_1512_02595_b200 import _lib, ctc
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    with open(os.path.join(ROOT, "include", "ds2ctc.h")) as f:
+        text = f.read()
+    return sorted(set(re.findall(r"\b(ds2ctc_[a-z_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.lib()
+    declared = header_functions()
+    assert declared, "no declarations parsed"
+    assert set(declared) == set(_lib.EXPORTS)
+    for name in declared:
+        assert hasattr(lib, name), f"{name} not exported"
+
+
+def test_version_and_status_strings():
+    lib = _lib.lib()
+    assert b"sm_100a" in lib.ds2ctc_version()
+    assert lib.ds2ctc_status_string(0) == b"no error"
+    assert lib.ds2ctc_status_string(1) == b"invalid value"
+
+
+def test_workspace_size_monotone():
+    a = ctc.workspace_size([40] * 16, [150] * 16, 29)
+    b = ctc.workspace_size([150] * 64, [700] * 64, 29)
+    c = ctc.workspace_size([60] * 64, [350] * 64, 6000)
+    assert 0 < a < b
+    # half-lattice store alone: sum S*(T+1) doubles
+    assert b >= 64 * 301 * 701 * 8
+    # the dense path also keeps compact occupancy rows
+    assert c >= 64 * 121 * 351 * 8 + 64 * 350 * 61 * 4
+    assert ctc.workspace_size([], [], 29) == 0
+
+
+def _call(acts_ptr=None, A=29, B=1, blank=28, labels=(1,), ll=(1,), il=(3,), costs_ptr=1, ws=256):
+    lib = _lib.lib()
+    P = ctypes.POINTER(ctypes.c_int)
+    lab = np.asarray(labels if len(labels) else [0], dtype=np.int32)
+    lla = np.asarray(ll if len(ll) else [0], dtype=np.int32)
+    ila = np.asarray(il if len(il) else [0], dtype=np.int32)
+    return lib.ds2ctc_compute_loss(acts_ptr, None, lab.ctypes.data_as(P), lla.ctypes.data_as(P),
+                                   ila.ctypes.data_as(P), A, B, blank, costs_ptr, ws, None)
+
+
+def test_invalid_values_rejected_without_gpu():
+    assert _call(A=1, blank=0) == 1                      # alphabet must include blank + 1 symbol
+    assert _call(blank=29) == 1                          # blank out of range
+    assert _call(blank=-1) == 1
+    assert _call(labels=(29,)) == 1                      # label out of range (reference UB; rejected)
+    assert _call(labels=(-2,)) == 1
+    assert _call(ll=(-1,)) == 1                          # negative lengths
+    assert _call(il=(-3,)) == 1
+    assert _call(B=-1) == 1
+    assert _call(acts_ptr=1, costs_ptr=None) == 1        # costs required
+    assert _call(acts_ptr=1, ws=None) == 1               # workspace required
+    assert _call(acts_ptr=1, ws=257) == 1                # 256-byte alignment
+
+
+def test_too_many_states_unsupported():
+    L = 2048  # 2L+1 = 4097 > DS2CTC_MAX_STATES
+    assert _call(labels=tuple([1] * L), ll=(L,), il=(5000,)) == 4
+    out = ctypes.c_size_t()
+    P = ctypes.POINTER(ctypes.c_int)
+    ll = np.asarray([L], dtype=np.int32)
+    il = np.asarray([5000], dtype=np.int32)
+    assert _lib.lib().ds2ctc_get_workspace_size(ll.ctypes.data_as(P), il.ctypes.data_as(P), 29, 1,
+                                                ctypes.byref(out)) == 4
+
+
+def test_empty_minibatch_is_noop():
+    # an empty data-parallel shard (trainer.cpp:141-155) must be a valid no-op
+    assert _call(B=0, labels=(), ll=(), il=()) == 0
+
+
+def test_checked_variant_rejects_small_workspace():
+    lib = _lib.lib()
+    P = ctypes.POINTER(ctypes.c_int)
+    lab = np.asarray([1, 2], dtype=np.int32)
+    ll = np.asarray([2], dtype=np.int32)
+    il = np.asarray([10], dtype=np.int32)
+    need = ctc.workspace_size(ll, il, 29)
+    st = lib.ds2ctc_compute_loss_checked(1, None, lab.ctypes.data_as(P), ll.ctypes.data_as(P), il.ctypes.data_as(P),
+                                         29, 1, 28, 1, 256, need - 1, None)
+    assert st == 1
+
+
+def test_missing_library_fails_loudly(monkeypatch):
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "LIB_PATH", "/nonexistent/libds2ctc.so")
+    with pytest.raises(ImportError):
+        _lib.lib()

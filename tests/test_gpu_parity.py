@@ -1,0 +1,123 @@
+"""GPU parity: the sm_100a path through the C-ABI vs the reference (golden
+fixtures made by the reference build) and the fp64 oracle restatement.
+
+Tolerances (BASELINE.json north_star): |cost - ref| / |ref| <= 1e-4 and
+max |grad - ref| <= 1e-4 in fp32; infeasible -> +inf cost and all-zero rows.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1512_02595_b200 import ctc as dctc
+from paper_1512_02595_b200.synth import fixed_shape_batch, make_batch, sortagrad_lengths
+
+from conftest import golden_cases
+
+pytestmark = pytest.mark.gpu
+
+COST_RTOL = 1e-4
+GRAD_ATOL = 1e-4
+
+
+def run_gpu(acts, flat, ll, il, blank=None, want_grad=True):
+    import torch
+
+    x = torch.from_numpy(np.ascontiguousarray(acts)).cuda()
+    costs, grads = dctc.compute_ctc_loss(x, flat, ll, il, blank=blank, want_grad=want_grad)
+    torch.cuda.synchronize()
+    return costs.cpu().numpy().astype(np.float64), (grads.cpu().numpy() if grads is not None else None)
+
+
+def assert_parity(costs, grads, ref_costs, ref_grads, il, what):
+    inf_ref = ~np.isfinite(ref_costs)
+    assert np.array_equal(~np.isfinite(costs), inf_ref), f"{what}: infeasible set differs {costs} {ref_costs}"
+    assert np.all(np.isposinf(costs[inf_ref])), f"{what}: infeasible must be +inf"
+    fin = ~inf_ref
+    if fin.any():
+        denom = np.maximum(np.abs(ref_costs[fin]), 1e-30)
+        rel = np.abs(costs[fin] - ref_costs[fin]) / denom
+        # loss can be ~0 (single forced path with p~1): fall back to absolute 1e-4 there
+        ok = (rel <= COST_RTOL) | (np.abs(costs[fin] - ref_costs[fin]) <= 1e-5)
+        assert ok.all(), f"{what}: cost rel err {rel.max():.3e}"
+    if grads is not None:
+        err = np.abs(grads.astype(np.float64) - ref_grads.astype(np.float64))
+        assert err.max() <= GRAD_ATOL, f"{what}: grad abs err {err.max():.3e}"
+        for b in np.where(inf_ref)[0]:
+            assert np.all(grads[:, b, :] == 0), f"{what}: infeasible utterance {b} has nonzero gradient"
+        for b in range(len(il)):
+            assert np.all(grads[il[b]:, b, :] == 0), f"{what}: padded frames of {b} not zero"
+
+
+def test_golden_cases(golden, cuda):
+    for name in golden_cases(golden):
+        acts = golden[f"{name}/acts"]
+        flat = golden[f"{name}/labels"]
+        ll = golden[f"{name}/label_lengths"]
+        il = golden[f"{name}/input_lengths"]
+        blank = int(golden[f"{name}/blank"])
+        if acts.shape[0] == 0:
+            continue
+        costs, grads = run_gpu(acts, flat, ll, il, blank=blank)
+        assert_parity(costs, grads, golden[f"{name}/costs"], golden[f"{name}/grads"], il, name)
+
+
+def test_cost_only_matches(golden, cuda):
+    name = "config1"
+    costs, grads = run_gpu(golden[f"{name}/acts"], golden[f"{name}/labels"], golden[f"{name}/label_lengths"],
+                           golden[f"{name}/input_lengths"], want_grad=False)
+    assert grads is None
+    ref = golden[f"{name}/costs"]
+    assert np.max(np.abs(costs - ref) / np.abs(ref)) <= COST_RTOL
+
+
+@pytest.mark.parametrize("shape", [("english", 29, 700, 150, 64), ("mandarin", 6000, 350, 60, 6)])
+def test_fixed_shapes_vs_oracle(cuda, shape):
+    name, A, T, L, B = shape
+    acts, flat, ll, il = fixed_shape_batch(A, T, L, B, seed=1234)
+    costs, grads = run_gpu(acts, flat, ll, il)
+    rc, rg = oracle.oracle_batch(acts, flat, ll, il, nthreads=8)
+    assert_parity(costs, grads, rc, rg, il, name)
+
+
+def test_peaked_english_vs_oracle(cuda):
+    acts, flat, ll, il = fixed_shape_batch(29, 700, 150, 8, seed=77, scale=8.0)
+    costs, grads = run_gpu(acts, flat, ll, il)
+    rc, rg = oracle.oracle_batch(acts, flat, ll, il, nthreads=8)
+    assert_parity(costs, grads, rc, rg, il, "peaked-english")
+
+
+def test_sortagrad_variable_vs_oracle(cuda):
+    T, L = sortagrad_lengths(24, seed=11)
+    acts, flat, ll, il = make_batch(29, T, L, seed=5)
+    costs, grads = run_gpu(acts, flat, ll, il)
+    rc, rg = oracle.oracle_batch(acts, flat, ll, il, nthreads=8)
+    assert_parity(costs, grads, rc, rg, il, "sortagrad")
+
+
+def test_gradient_rows_sum_to_zero_full_size(cuda):
+    # sum_c softmax - sum_c occupancy = 1 - 1 per live frame (size-independent property)
+    acts, flat, ll, il = fixed_shape_batch(29, 700, 150, 64, seed=3)
+    costs, grads = run_gpu(acts, flat, ll, il)
+    assert np.all(np.isfinite(costs))
+    assert np.abs(grads.astype(np.float64).sum(axis=2)).max() < 1e-4
+
+
+def test_deterministic(cuda):
+    acts, flat, ll, il = fixed_shape_batch(29, 300, 80, 16, seed=9)
+    c1, g1 = run_gpu(acts, flat, ll, il)
+    c2, g2 = run_gpu(acts, flat, ll, il)
+    assert np.array_equal(c1, c2) and np.array_equal(g1, g2)
+
+
+def test_host_api_and_single_utterance(golden, cuda):
+    name = "config1"
+    acts = golden[f"{name}/acts"]
+    flat = golden[f"{name}/labels"]
+    ll = golden[f"{name}/label_lengths"]
+    il = golden[f"{name}/input_lengths"]
+    costs, grads = dctc.compute_ctc_loss_host(acts, flat, ll, il)
+    assert_parity(costs.astype(np.float64), grads, golden[f"{name}/costs"], golden[f"{name}/grads"], il, "host")
+    res = dctc.ctc_loss(acts[:, 0, :], flat[:ll[0]], blank=28)
+    assert res.feasible
+    assert abs(res.loss - golden[f"{name}/costs"][0]) / golden[f"{name}/costs"][0] <= COST_RTOL
+    assert np.abs(res.logit_grad - golden[f"{name}/grads"][:, 0, :]).max() <= GRAD_ATOL
