@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""Benchmark of the DS2 CTC loss + gradient hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload english]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+    python bench.py --impl reference ...     # the reference CPU CTC arm
+
+A "step" is one pass of the CTC hot path over one global minibatch that is
+already resident in HBM: ds2ctc_compute_loss (logit stats -> alpha||beta
+pair chain with the fused gradient [-> dense gradient]) + the trainer's
+{sum loss, #skipped} reduction (ds2ctc_loss_sum) + for N > 1 one NCCL
+all-reduce of those two fp64 scalars (trainer.cpp:174-180). Each GPU owns
+its LPT shard of the global minibatch (H1 scheduler).
+
+Timing: W untimed warm-up steps (plus an untimed soak of ~0.5 s so clocks
+settle and nvidia-smi sees load), then EXACTLY K steps, each bracketed by
+CUDA events on the launching stream, with a 256 MiB memset between steps to
+flush L2 (the English inputs are 5 MB and would otherwise stay L2-resident);
+barrier + synchronize around the timed region; max over ranks. `e2e` is the
+same metric through the host-buffer C-ABI call (pinned host activations in,
+gradients + costs out, copies inside the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1512_02595_b200.synth import make_batch, sortagrad_lengths  # noqa: E402
+
+METRIC = "CTC loss+grad utterances/sec"
+UNIT = "utt/s"
+
+WORKLOADS = {
+    # BASELINE.json configs[1]: the headline (fits one GPU; weak scaling, 64 utterances per GPU)
+    "english": dict(A=29, T=700, L=150, per_gpu=64, scaling="weak",
+                    desc="English DS2 shape A=29 T=700 L=150, 64 utterances per GPU"),
+    "config1": dict(A=29, T=150, L=40, per_gpu=16, scaling="weak", desc="configs[0] A=29 T=150 L=40 B=16 per GPU"),
+    "mandarin": dict(A=6000, T=350, L=60, per_gpu=64, scaling="weak",
+                     desc="Mandarin DS2 shape A=6000 T=350 L=60, 64 utterances per GPU"),
+    "sortagrad": dict(A=29, total=512, scaling="strong",
+                      desc="SortaGrad batch T~U[50,1500] L~U[5,min(300,T/2)] B=512 sharded over N GPUs"),
+    "edge1500": dict(A=29, T=1500, L=300, total=1024, scaling="strong",
+                     desc="B=1024 at T=1500 L=300 sharded over N GPUs"),
+}
+
+
+def global_batch(wl: dict, n_gpus: int, seed: int = 1234):
+    """(input_lengths, label_lengths) of the global minibatch."""
+    if "per_gpu" in wl:
+        B = wl["per_gpu"] * n_gpus
+        return np.full(B, wl["T"], np.int32), np.full(B, wl["L"], np.int32)
+    if "T" in wl:
+        return np.full(wl["total"], wl["T"], np.int32), np.full(wl["total"], wl["L"], np.int32)
+    T, L = sortagrad_lengths(wl["total"], seed=7)
+    order = np.argsort(T, kind="stable")  # one SortaGrad (epoch 0) minibatch
+    return T[order], L[order]
+
+
+def shard_inputs(wl, il_g, ll_g, idx, rank, seed=1234):
+    """Synthetic logits N(0,1) (reference Rng stream) for this rank's utterances."""
+    il = il_g[idx]
+    ll = ll_g[idx]
+    acts, flat, ll, il = make_batch(wl["A"], il, ll, seed=seed + 7919 * rank)
+    return acts, flat, ll, il
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling in the background (B200_PROFILING.md recipe)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.proc = None
+        self.t0 = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", ",".join(str(g) for g in gpus), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sms, maxs, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm, mx, util = float(parts[1]), float(parts[2]), float(parts[3])
+            except ValueError:
+                continue
+            if util <= 0:
+                continue
+            sms.append(sm)
+            maxs.append(mx)
+            for name, flag in zip(names, parts[5:9]):
+                if flag.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": max(maxs) if maxs else None,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def cpu_reference_rate(acts, flat, ll, il, nthreads, min_seconds):
+    """The reference's own ctc_loss_reference (oracle/_ref build) on host cores; utt/s."""
+    import oracle
+
+    kind = "reference" if oracle.ref_available() else "port"
+    fn = oracle.ref_batch if kind == "reference" else oracle.oracle_batch
+    fn(acts[:, :min(4, acts.shape[1]), :], flat[:int(ll[:4].sum())], ll[:4], il[:4], nthreads=nthreads)  # warm
+    done = 0
+    t0 = time.perf_counter()
+    while True:
+        fn(acts, flat, ll, il, nthreads=nthreads)
+        done += ll.shape[0]
+        el = time.perf_counter() - t0
+        if el >= min_seconds:
+            break
+    return done / el, kind, done, el
+
+
+def run_reference(args, wl):
+    """--impl reference: the reference CPU CTC with all host threads (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+
+    il_g, ll_g = global_batch(wl, 1)
+    n = min(64, il_g.shape[0])
+    acts, flat, ll, il = shard_inputs(wl, il_g, ll_g, np.arange(n), 0)
+    nthreads = os.cpu_count() or 1
+    kind = "reference" if oracle.ref_available() else "port"
+    fn = oracle.ref_batch if kind == "reference" else oracle.oracle_batch
+    for _ in range(max(args.warmup, 1)):
+        fn(acts, flat, ll, il, nthreads=nthreads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        fn(acts, flat, ll, il, nthreads=nthreads)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * statistics.mean(times)
+    value = n / (ms / 1e3)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": wl["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "desc": wl["desc"], "utterances_per_step": n,
+                   "frames_per_step": int(il.sum())},
+        "frames_per_s": float(il.sum()) / (ms / 1e3),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": kind,
+                         "sample": f"{n} utterances of the {args.workload} workload per step, "
+                                   f"asr::ctc::ctc_loss_reference fp64, one utterance per thread"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="english", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--soak-seconds", type=float, default=0.5)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, wl)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1512_02595_b200 import _lib, ctc, scheduler
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _lib.lib()
+
+    il_g, ll_g = global_batch(wl, world)
+    idx = scheduler.shard_batch(il_g, ll_g, wl["A"], world, rank)
+    acts_h, flat, ll, il = shard_inputs(wl, il_g, ll_g, idx, rank)
+    B = int(ll.shape[0])
+    A = wl["A"]
+    x = torch.from_numpy(acts_h).to(dev)
+    grads = torch.empty_like(x)
+    costs = torch.empty(max(B, 1), dtype=torch.float32, device=dev)
+    pair = torch.zeros(2, dtype=torch.float64, device=dev)
+    ws = ctc.Workspace(dev)
+    ws_ptr, ws_bytes = ws.get(ctc.workspace_size(ll, il, A))
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    P = ctypes.POINTER(ctypes.c_int)
+    lab_c = np.ascontiguousarray(flat if flat.size else np.zeros(1, np.int32), dtype=np.int32)
+    ll_c = np.ascontiguousarray(ll if B else np.zeros(1, np.int32), dtype=np.int32)
+    il_c = np.ascontiguousarray(il if B else np.zeros(1, np.int32), dtype=np.int32)
+    launches_per_step = 0
+
+    def step():
+        st = lib.ds2ctc_compute_loss_checked(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(grads.data_ptr()),
+                                             lab_c.ctypes.data_as(P), ll_c.ctypes.data_as(P),
+                                             il_c.ctypes.data_as(P), A, B, A - 1, ctypes.c_void_p(costs.data_ptr()),
+                                             ctypes.c_void_p(ws_ptr), ws_bytes, ctypes.c_void_p(stream.cuda_stream))
+        _lib.check(st, "ds2ctc_compute_loss")
+        _lib.check(lib.ds2ctc_loss_sum(ctypes.c_void_p(costs.data_ptr()), B, ctypes.c_void_p(pair.data_ptr()),
+                                       ctypes.c_void_p(stream.cuda_stream)), "ds2ctc_loss_sum")
+        if world > 1:
+            dist.all_reduce(pair)
+
+    # kernels of ours per step: k_pair (+ k_dense + k_finalize for large A) + k_loss_sum
+    if B:
+        launches_per_step = 1 + (2 if A > 128 else 0) + 1
+    else:
+        launches_per_step = 1
+
+    sampler = ClockSampler([local_rank]) if rank == 0 else None
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < args.soak_seconds:
+        flush.zero_()
+        step()
+        torch.cuda.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    stage = np.zeros((args.steps, 4), dtype=np.float64)
+    ms4 = (ctypes.c_float * 4)()
+    lib.ds2ctc_profile_enable(args.steps if B else 0)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush.zero_()
+        starts[k].record(stream)
+        step()
+        ends[k].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    for k in range(args.steps if B else 0):
+        _lib.check(lib.ds2ctc_profile_read(k, ms4), "ds2ctc_profile_read")
+        stage[k] = list(ms4)
+    lib.ds2ctc_profile_enable(0)
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms_local = statistics.mean(step_ms)
+    pair_ms_local = float(stage[:, 0].mean()) if B else 0.0
+    dense_ms_local = float(stage[:, 1].mean()) if B else 0.0
+    final_ms_local = float(stage[:, 2].mean()) if B else 0.0
+
+    # ---- e2e through the host-buffer C-ABI (pinned host buffers, copies timed) ----
+    acts_pin = torch.from_numpy(acts_h).pin_memory()
+    grads_pin = torch.empty(acts_h.shape, dtype=torch.float32).pin_memory()
+    costs_pin = torch.empty(max(B, 1), dtype=torch.float32).pin_memory()
+
+    def e2e_call():
+        if B == 0:
+            return
+        st = lib.ds2ctc_compute_loss_host(ctypes.c_void_p(acts_pin.data_ptr()), ctypes.c_void_p(grads_pin.data_ptr()),
+                                          lab_c.ctypes.data_as(P), ll_c.ctypes.data_as(P), il_c.ctypes.data_as(P),
+                                          A, B, A - 1, ctypes.c_void_p(costs_pin.data_ptr()), local_rank)
+        _lib.check(st, "ds2ctc_compute_loss_host")
+
+    for _ in range(args.warmup):
+        e2e_call()
+    if world > 1:
+        dist.barrier()
+    e2e_times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        e2e_call()
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_ms_local = 1e3 * statistics.mean(e2e_times)
+
+    # ---- max over ranks ----
+    vals = torch.tensor([ms_local, pair_ms_local, e2e_ms_local, dense_ms_local, final_ms_local],
+                        dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    ms, pair_ms, e2e_ms, dense_ms, final_ms = [float(v) for v in vals.cpu()]
+    total_utts = int(il_g.shape[0])
+    total_frames = int(il_g.sum())
+    value = total_utts / (ms / 1e3)
+    # loss check (parity is the test suite's job; this guards the bench itself)
+    torch.cuda.synchronize()
+    loss_sum, skipped = [float(v) for v in pair.cpu()]
+
+    if rank == 0:
+        peak, peak_kind = load_peaks()
+        # Algorithmic bytes of the path: activations read once + gradients
+        # written once (8*T*A per utterance) + labels and lengths. Attributed to the dominant
+        # kernel: k_pair for small alphabets (it reads the logits and writes the gradient),
+        # k_dense for large ones (the HBM pass).
+        alg_bytes = 8.0 * float((il.astype(np.float64) * A).sum()) + 4.0 * float(ll.sum()) + 8.0 * B
+        dom_name, dom_ms = ("k_pair", pair_ms) if pair_ms >= dense_ms else ("k_dense", dense_ms)
+        achieved = alg_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath):
+            try:
+                with open(tpath) as f:
+                    traffic = json.load(f).get(args.workload)
+            except Exception:
+                traffic = None
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": wl["scaling"],
+            "vs_baseline": None, "dtype": "f32 in/out, f64 lattice carry", "data": "synthetic",
+            "config": {"workload": args.workload, "desc": wl["desc"], "alphabet": A,
+                       "global_batch": total_utts, "frames_per_step": total_frames,
+                       "parallelism": f"dp{world}", "l2": "flushed between steps (256 MiB memset)"},
+            "frames_per_s": total_frames / (ms / 1e3),
+            "stage_ms": {"k_pair": pair_ms, "k_dense": dense_ms, "k_finalize": final_ms},
+            "roofline": {"bound": "hbm", "kernel": dom_name, "kernel_ms": dom_ms, "achieved": achieved, "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "alg_bytes_per_launch": alg_bytes},
+            "e2e": {"value": total_utts / (e2e_ms / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": int(acts_h.nbytes + 4 * (ll.sum() + 2 * B)),
+                    "d2h_bytes_per_step": int(acts_h.nbytes + 4 * B), "ms_per_step": e2e_ms},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks,
+            "loss_sum": loss_sum, "skipped": int(skipped),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            n = min(64, B)
+            sub = np.arange(n)
+            rate, kind, done, el = cpu_reference_rate(acts_h[:, sub, :], flat[:int(ll[:n].sum())], ll[:n], il[:n],
+                                                      os.cpu_count() or 1, args.cpu_seconds)
+            line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": kind,
+                                    "sample": f"{done} utterances ({n} per batch) of the {args.workload} "
+                                              f"workload in {el:.1f} s, asr::ctc::ctc_loss_reference fp64, "
+                                              f"one utterance per thread"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -106,6 +106,27 @@ ds2ctc_status ds2ctc_compute_loss_host(const float* activations, float* gradient
                                        const int* label_lengths, const int* input_lengths, int alphabet_size,
                                        int minibatch, int blank_label, float* costs, int device);
 
+/*
+ * Per-shard {sum of feasible costs, number of infeasible utterances} as fp64
+ * [2] on the device, the two scalars train_epoch accumulates
+ * (local_loss / local_skipped, trainer.cpp:160-168) and all-reduces
+ * (trainer.cpp:176-179). Fixed summation order (deterministic). costs and
+ * out2 are DEVICE pointers; asynchronous on `stream`.
+ */
+ds2ctc_status ds2ctc_loss_sum(const float* costs, int minibatch, double* out2, void* stream);
+
+/*
+ * Stage timing for benchmarks: when enabled for the calling thread with
+ * `slots` > 0, each compute call records CUDA events on its stream around
+ * every kernel of the pipeline into the next of `slots` event sets (no host
+ * synchronisation). ds2ctc_profile_read(i) synchronises on call i (counted
+ * from the enable, i < slots) and writes ms[4] = {pair kernel (alpha||beta
+ * chain, fused gradient), dense gradient pass, cost finalisation, whole
+ * call}. slots == 0 disables.
+ */
+ds2ctc_status ds2ctc_profile_enable(int slots);
+ds2ctc_status ds2ctc_profile_read(int call_index, float* ms);
+
 /* ---------------------------------------------------------------------
  * H1 host scheduler (trainer.cpp:58-91, 140-143) -- pure host functions.
  * ------------------------------------------------------------------- */

@@ -1,0 +1,107 @@
+// ds2ctc.hpp -- header-only C++ shim over the C-ABI with the reference's
+// own CTC signature, so reference-style callers and tests can switch
+// implementations by name:
+//
+//   asr::ctc::CtcResult asr::ctc::ctc_loss_reference(const Matrix& frame_logits,
+//                                                    const std::vector<int>& label, int blank);
+//   (/root/reference/proj/include/asr/ctc.hpp:84-87)
+//
+//   template <class M> ds2ctc::CtcResult<M> ds2ctc::ctc_loss_gpu(const M& frame_logits,
+//                                                            const std::vector<int>& label, int blank);
+//
+// M is any row-major matrix type with rows(), cols(), operator()(r, c) and a
+// (rows, cols) constructor -- asr::Matrix qualifies unchanged. The result
+// mirrors asr::ctc::CtcResult (ctc.hpp:62-66): feasible, loss = -log p,
+// logit_grad T x A (empty when infeasible). Computation runs on `device`
+// through ds2ctc_compute_loss_host (fp32 in/out, fp64 lattice carry).
+//
+// ctc_loss_batch_gpu is the batched form the trainer loop
+// (proj/src/trainer.cpp:155-171) maps onto: one call for the whole local
+// minibatch instead of one ctc_loss_reference per utterance, with the
+// trainer's convention already applied (infeasible -> zero gradient).
+#ifndef DS2CTC_HPP
+#define DS2CTC_HPP
+
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ds2ctc.h"
+
+namespace ds2ctc {
+
+template <class M>
+struct CtcResult {
+  bool feasible = false;
+  double loss = std::numeric_limits<double>::infinity();
+  M logit_grad;  // T x A; empty when infeasible
+};
+
+inline void check(ds2ctc_status st, const char* where) {
+  if (st != DS2CTC_STATUS_SUCCESS)
+    throw std::runtime_error(std::string("ds2ctc: ") + where + ": " + ds2ctc_status_string(st));
+}
+
+template <class M>
+CtcResult<M> ctc_loss_gpu(const M& frame_logits, const std::vector<int>& label, int blank, int device = 0) {
+  const int T = frame_logits.rows();
+  const int A = frame_logits.cols();
+  std::vector<float> x(static_cast<size_t>(T) * A), g(x.size());
+  for (int t = 0; t < T; ++t)
+    for (int k = 0; k < A; ++k) x[static_cast<size_t>(t) * A + k] = static_cast<float>(frame_logits(t, k));
+  const int L = static_cast<int>(label.size());
+  float cost = 0.f;
+  check(ds2ctc_compute_loss_host(x.data(), g.data(), label.data(), &L, &T, A, 1, blank, &cost, device),
+        "ctc_loss_gpu");
+  CtcResult<M> res;
+  if (!std::isfinite(cost)) return res;
+  res.feasible = true;
+  res.loss = cost;
+  res.logit_grad = M(T, A);
+  for (int t = 0; t < T; ++t)
+    for (int k = 0; k < A; ++k) res.logit_grad(t, k) = g[static_cast<size_t>(t) * A + k];
+  return res;
+}
+
+// Batched: logits[i] is T_i x A. Returns per-utterance costs (+inf when
+// infeasible) and fills dlogits[i] (T_i x A, zero when infeasible).
+template <class M>
+std::vector<double> ctc_loss_batch_gpu(const std::vector<M>& logits, const std::vector<std::vector<int>>& labels,
+                                       int blank, std::vector<M>* dlogits, int device = 0) {
+  const int B = static_cast<int>(logits.size());
+  if (B == 0) return {};
+  const int A = logits[0].cols();
+  std::vector<int> il(B), ll(B), flat;
+  int t_max = 0;
+  for (int b = 0; b < B; ++b) {
+    il[b] = logits[b].rows();
+    ll[b] = static_cast<int>(labels[b].size());
+    t_max = std::max(t_max, il[b]);
+    flat.insert(flat.end(), labels[b].begin(), labels[b].end());
+  }
+  std::vector<float> x(static_cast<size_t>(t_max) * B * A, 0.f), g(dlogits ? x.size() : 0);
+  for (int b = 0; b < B; ++b)
+    for (int t = 0; t < il[b]; ++t)
+      for (int k = 0; k < A; ++k) x[(static_cast<size_t>(t) * B + b) * A + k] = static_cast<float>(logits[b](t, k));
+  std::vector<float> costs(B);
+  check(ds2ctc_compute_loss_host(x.data(), dlogits ? g.data() : nullptr, flat.data(), ll.data(), il.data(), A, B,
+                                 blank, costs.data(), device),
+        "ctc_loss_batch_gpu");
+  if (dlogits) {
+    dlogits->clear();
+    for (int b = 0; b < B; ++b) {
+      M d(il[b], A);
+      for (int t = 0; t < il[b]; ++t)
+        for (int k = 0; k < A; ++k) d(t, k) = g[(static_cast<size_t>(t) * B + b) * A + k];
+      dlogits->push_back(std::move(d));
+    }
+  }
+  return std::vector<double>(costs.begin(), costs.end());
+}
+
+}  // namespace ds2ctc
+
+#endif  // DS2CTC_HPP

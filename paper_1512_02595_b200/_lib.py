@@ -29,6 +29,9 @@ EXPORTS = (
     "ds2ctc_compute_loss",
     "ds2ctc_compute_loss_checked",
     "ds2ctc_compute_loss_host",
+    "ds2ctc_loss_sum",
+    "ds2ctc_profile_enable",
+    "ds2ctc_profile_read",
     "ds2ctc_sortagrad_order",
     "ds2ctc_rank_slice",
     "ds2ctc_shard_lpt",
@@ -77,6 +80,12 @@ def lib():
             L.ds2ctc_compute_loss_host.restype = ctypes.c_int
             L.ds2ctc_compute_loss_host.argtypes = [_p, _p, _ip, _ip, _ip, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                                    _p, ctypes.c_int]
+            L.ds2ctc_loss_sum.restype = ctypes.c_int
+            L.ds2ctc_loss_sum.argtypes = [_p, ctypes.c_int, _p, _p]
+            L.ds2ctc_profile_enable.restype = ctypes.c_int
+            L.ds2ctc_profile_enable.argtypes = [ctypes.c_int]
+            L.ds2ctc_profile_read.restype = ctypes.c_int
+            L.ds2ctc_profile_read.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_float)]
             L.ds2ctc_sortagrad_order.restype = ctypes.c_int
             L.ds2ctc_sortagrad_order.argtypes = [_ip, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_uint64,
                                                  ctypes.c_int, _i64p]

@@ -65,6 +65,39 @@ Staging& staging_for_current_device() {
   return per_device[dev];
 }
 
+// Optional per-thread stage timing (ds2ctc_profile_enable / _read): a ring
+// of event sets so timed calls never synchronise the host.
+struct Profiler {
+  int slots = 0;
+  int device = -1;
+  long long calls = 0;
+  std::vector<cudaEvent_t> ev;  // 4 per slot
+  void reset() {
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    ev.clear();
+    calls = 0;
+    device = -1;
+  }
+  bool ready(int dev) {
+    if (slots <= 0) return false;
+    if (device != dev || static_cast<int>(ev.size()) != 4 * slots) {
+      reset();
+      ev.assign(4 * slots, nullptr);
+      for (auto& e : ev)
+        if (cudaEventCreate(&e) != cudaSuccess) return false;
+      device = dev;
+    }
+    return calls < slots;
+  }
+  void mark(int i, cudaStream_t s) { cudaEventRecord(ev[4 * calls + i], s); }
+};
+
+Profiler& profiler() {
+  thread_local Profiler p;
+  return p;
+}
+
 int min_frames(const int* label, int L) {  // ctc.cpp:102-107
   int needed = L;
   for (int i = 1; i < L; ++i)
@@ -89,20 +122,23 @@ ds2ctc_status validate(const int* label_lengths, const int* input_lengths, int A
 }
 
 // Builds the metadata blob (int32 words laid out per Layout) into `blob`.
-// Returns the max S over utterances that run the lattice.
-int build_metadata(const Layout& lay, const int* flat_labels, const int* label_lengths, const int* input_lengths,
-                   int B, int blank, std::vector<int32_t>& blob) {
+// Returns (max L, max nkey) over utterances that run the lattice.
+std::pair<int, int> build_metadata(const Layout& lay, const int* flat_labels, const int* label_lengths,
+                                   const int* input_lengths, int B, int blank, std::vector<int32_t>& blob) {
   blob.assign(lay.meta_end / sizeof(int32_t), 0);
   auto* desc = reinterpret_cast<UttDesc*>(blob.data() + lay.desc / 4);
   int* order = blob.data() + lay.order / 4;
   int* labels = blob.data() + lay.labels / 4;
   int* key_char = blob.data() + lay.key_char / 4;
   int* key_start = blob.data() + lay.key_start / 4;
-  int* key_rows = blob.data() + lay.key_rows / 4;
+  int* key_pos = blob.data() + lay.key_pos / 4;
   if (lay.sum_L > 0) std::memcpy(labels, flat_labels, sizeof(int) * lay.sum_L);
 
+  int max_L_all = 0;
+  for (int b = 0; b < B; ++b) max_L_all = std::max(max_L_all, label_lengths[b]);
+  const int K = pick_K(max_L_all);
   long long lab_off = 0, key_off = 0, store_off = 0, occ_off = 0;
-  int max_S = 1;
+  int max_L = 0, max_nkey = 1;
   std::vector<std::pair<int, int>> kv;
   for (int b = 0; b < B; ++b) {
     UttDesc& u = desc[b];
@@ -113,16 +149,17 @@ int build_metadata(const Layout& lay, const int* flat_labels, const int* label_l
     u.S = 2 * L + 1;
     u.status = T < min_frames(lab, L) ? 1 : (T == 0 ? 2 : 0);
     u.lab_off = static_cast<int>(lab_off);
-    u.row_off = static_cast<int>(lab_off);
     u.key_off = static_cast<int>(key_off);
+    u.col_w = column_width(L, K);
     u.store_off = store_off;
     u.occ_off = occ_off;
     u.tm = T > 0 ? (T - 1) / 2 : 0;
-    // Key groups (ctc.cpp:47-66): slot 0 = blank (even rows are summed on the
-    // device; only odd rows whose label equals the blank id are listed),
-    // slots 1.. = distinct non-blank symbols ascending, rows ascending.
+    // Key groups (group_rows_by_key, ctc.cpp:47-66) over label positions:
+    // slot 0 = blank (all even lattice rows, plus label positions whose symbol
+    // is the blank id), slots 1.. = distinct non-blank symbols ascending,
+    // positions ascending within a slot.
     kv.clear();
-    for (int i = 0; i < L; ++i) kv.emplace_back(lab[i] == blank ? -1 : lab[i], 2 * i + 1);
+    for (int i = 0; i < L; ++i) kv.emplace_back(lab[i] == blank ? -1 : lab[i], i);
     std::sort(kv.begin(), kv.end());
     int nkey = 1;
     key_char[key_off] = blank;
@@ -130,29 +167,32 @@ int build_metadata(const Layout& lay, const int* flat_labels, const int* label_l
     ks[0] = 0;
     int r = 0;
     size_t i = 0;
-    while (i < kv.size() && kv[i].first == -1) key_rows[lab_off + r++] = kv[i++].second;
+    while (i < kv.size() && kv[i].first == -1) key_pos[lab_off + r++] = kv[i++].second;
     ks[1] = r;
     while (i < kv.size()) {
       const int sym = kv[i].first;
       key_char[key_off + nkey] = sym;
-      while (i < kv.size() && kv[i].first == sym) key_rows[lab_off + r++] = kv[i++].second;
+      while (i < kv.size() && kv[i].first == sym) key_pos[lab_off + r++] = kv[i++].second;
       ks[++nkey] = r;
     }
     u.nkey = nkey;
-    if (u.status == 0) max_S = std::max(max_S, u.S);
+    if (u.status == 0) {
+      max_L = std::max(max_L, L);
+      max_nkey = std::max(max_nkey, nkey);
+    }
     lab_off += L;
     key_off += L + 1;
-    store_off += static_cast<long long>(u.S) * (T + 1);
-    occ_off += static_cast<long long>(T) * (L + 1);
+    store_off += static_cast<long long>(u.col_w) * (T + 1);
+    occ_off += static_cast<long long>(T) * nkey;
   }
-  // Longest first (the serial chain is ~T steps), so long pairs start in the first wave.
+  // Longest first (the serial chain is T steps), so long pairs start in the first wave.
   std::iota(order, order + B, 0);
   std::stable_sort(order, order + B, [&](int x, int y) {
     const int tx = desc[x].status == 0 ? desc[x].T : -1;
     const int ty = desc[y].status == 0 ? desc[y].T : -1;
     return tx > ty;
   });
-  return max_S;
+  return {max_L, max_nkey};
 }
 
 ds2ctc_status run(const float* acts, float* grads, const int* flat_labels, const int* label_lengths,
@@ -168,7 +208,7 @@ ds2ctc_status run(const float* acts, float* grads, const int* flat_labels, const
   if (reinterpret_cast<uintptr_t>(workspace) % kAlign != 0) return DS2CTC_STATUS_INVALID_VALUE;
 
   thread_local std::vector<int32_t> blob;
-  const int max_S = build_metadata(lay, flat_labels, label_lengths, input_lengths, B, blank, blob);
+  const auto mx = build_metadata(lay, flat_labels, label_lengths, input_lengths, B, blank, blob);
 
   auto* ws = static_cast<unsigned char*>(workspace);
   auto s = static_cast<cudaStream_t>(stream);
@@ -180,7 +220,8 @@ ds2ctc_status run(const float* acts, float* grads, const int* flat_labels, const
     return DS2CTC_STATUS_MEMOPS_FAILED;
   if (cudaEventRecord(ev, s) != cudaSuccess) return DS2CTC_STATUS_MEMOPS_FAILED;
 
-  ChainArgs a{};
+  const bool fused = A <= kFusedMaxAlphabet;
+  PairArgs a{};
   a.x = acts;
   a.grad = grads;
   a.costs = costs;
@@ -189,23 +230,33 @@ ds2ctc_status run(const float* acts, float* grads, const int* flat_labels, const
   a.labels = reinterpret_cast<const int*>(ws + lay.labels);
   a.key_char = reinterpret_cast<const int*>(ws + lay.key_char);
   a.key_start = reinterpret_cast<const int*>(ws + lay.key_start);
-  a.key_rows = reinterpret_cast<const int*>(ws + lay.key_rows);
-  a.stats = reinterpret_cast<const float2*>(ws + lay.stats);
-  a.store = reinterpret_cast<double*>(ws + lay.store);
-  a.occ = (grads != nullptr && A > kFusedMaxAlphabet) ? reinterpret_cast<float*>(ws + lay.occ) : nullptr;
+  a.key_pos = reinterpret_cast<const int*>(ws + lay.key_pos);
+  a.store = reinterpret_cast<float*>(ws + lay.store);
+  a.occ = fused ? nullptr : reinterpret_cast<float*>(ws + lay.occ);
+  a.lse = fused ? nullptr : reinterpret_cast<float2*>(ws + lay.lse);
   a.logz = reinterpret_cast<double*>(ws + lay.logz);
+  a.part = reinterpret_cast<double*>(ws + lay.part);
   a.t_max = lay.t_max;
   a.B = B;
   a.A = A;
   a.blank = blank;
-  int nt = std::min(1024, (max_S + 31) / 32 * 32);
-  if (grads != nullptr && A <= kFusedMaxAlphabet) nt = std::max(nt, (A + 31) / 32 * 32);
-  a.nthreads = std::max(nt, 32);
-  a.cells = (max_S + a.nthreads - 1) / a.nthreads;
+  a.g = make_geometry(mx.first, mx.second, A, fused);
+  if (static_cast<size_t>(a.g.smem) > kSmemBudget) return DS2CTC_STATUS_UNSUPPORTED;
 
-  if (launch_rowstats(a, stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
-  if (launch_chain(a, stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
-  if (a.occ != nullptr && launch_dense(a, stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Profiler& prof = profiler();
+  const bool timed = prof.ready(dev);
+  if (timed) prof.mark(0, s);
+  if (launch_pair(a, stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  if (timed) prof.mark(1, s);
+  if (!fused && launch_dense(a, grads != nullptr, stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  if (timed) prof.mark(2, s);
+  if (!fused && launch_finalize(a, stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  if (timed) {
+    prof.mark(3, s);
+    ++prof.calls;
+  }
   return DS2CTC_STATUS_SUCCESS;
 }
 
@@ -288,6 +339,33 @@ ds2ctc_status ds2ctc_compute_loss_checked(const float* activations, float* gradi
                                           size_t workspace_bytes, void* stream) {
   return run(activations, gradients, flat_labels, label_lengths, input_lengths, alphabet_size, minibatch,
              blank_label, costs, workspace, workspace_bytes, true, stream);
+}
+
+ds2ctc_status ds2ctc_loss_sum(const float* costs, int minibatch, double* out2, void* stream) {
+  if (minibatch < 0 || out2 == nullptr || (minibatch > 0 && costs == nullptr)) return DS2CTC_STATUS_INVALID_VALUE;
+  if (launch_loss_sum(costs, minibatch, out2, stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  return DS2CTC_STATUS_SUCCESS;
+}
+
+ds2ctc_status ds2ctc_profile_enable(int slots) {
+  if (slots < 0) return DS2CTC_STATUS_INVALID_VALUE;
+  Profiler& p = profiler();
+  p.reset();
+  p.slots = slots;
+  return DS2CTC_STATUS_SUCCESS;
+}
+
+ds2ctc_status ds2ctc_profile_read(int call_index, float* ms) {
+  Profiler& p = profiler();
+  if (ms == nullptr || call_index < 0 || call_index >= p.calls) return DS2CTC_STATUS_INVALID_VALUE;
+  cudaEvent_t* e = p.ev.data() + 4 * call_index;
+  if (cudaEventSynchronize(e[3]) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  if (cudaEventElapsedTime(&ms[0], e[0], e[1]) != cudaSuccess ||
+      cudaEventElapsedTime(&ms[1], e[1], e[2]) != cudaSuccess ||
+      cudaEventElapsedTime(&ms[2], e[2], e[3]) != cudaSuccess ||
+      cudaEventElapsedTime(&ms[3], e[0], e[3]) != cudaSuccess)
+    return DS2CTC_STATUS_EXECUTION_FAILED;
+  return DS2CTC_STATUS_SUCCESS;
 }
 
 ds2ctc_status ds2ctc_compute_loss_host(const float* activations, float* gradients, const int* flat_labels,

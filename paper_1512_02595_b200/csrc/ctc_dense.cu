@@ -1,0 +1,217 @@
+// ctc_dense.cu -- large-alphabet gradient pass, cost finalisation and the
+// trainer's scalar reduction (sm_100a).
+//
+// k_dense: one CTA per frame row (t, b), one read of the logits and one
+// write of the gradient: the row's max and log-sum-exp (log_softmax_rows,
+// ctc.cpp:24-37) and g = softmax - occupancy (grad_column, ctc.cpp:69-79),
+// where the occupancy is scattered only to the <= L+1 label symbols of the
+// utterance (a per-row bitmap of the key symbols + the compact occupancy row
+// written by k_pair), never densely. HBM-bound: 8*A bytes per row.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ds2ctc_internal.h"
+
+namespace ds2ctc {
+namespace {
+
+constexpr double kLn2 = 0.69314718055994530942;
+constexpr int kDenseThreads = 256;
+constexpr int kDenseVec = 8;  // float4 per thread in registers -> A <= 8192 on the vector path
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float4 ldg_stream(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void stg_stream(float4* p, float4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+
+// Block-wide max and sum (deterministic order: warp xor tree, then warps in order).
+__device__ __forceinline__ float block_max(float v, float* sh) {
+  v = warp_max(v);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float m = sh[0];
+  for (int w = 1; w < kDenseThreads / 32; ++w) m = fmaxf(m, sh[w]);
+  __syncthreads();
+  return m;
+}
+
+__device__ __forceinline__ float block_sum(float v, float* sh) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float s = 0.f;
+  for (int w = 0; w < kDenseThreads / 32; ++w) s += sh[w];
+  __syncthreads();
+  return s;
+}
+
+__global__ void __launch_bounds__(kDenseThreads) k_dense(PairArgs a, int write_grad) {
+  __shared__ float sh[32];
+  __shared__ unsigned bits[kDenseVec * kDenseThreads * 4 / 32];
+  __shared__ int nkey_s;
+  const int row = blockIdx.x;
+  const int t = row / a.B;
+  const int b = row - t * a.B;
+  const UttDesc u = a.desc[b];
+  const int A = a.A;
+  const int tid = threadIdx.x;
+  float* gr = write_grad ? a.grad + static_cast<size_t>(row) * A : nullptr;
+  const float* xr = a.x + static_cast<size_t>(row) * A;
+  const bool live = u.status == 0 && t < u.T && a.logz[b] != -__builtin_huge_val();
+  if (!live) {
+    if (gr)
+      for (int c = tid; c < A; c += kDenseThreads) gr[c] = 0.f;
+    return;
+  }
+  const int* keys = a.key_char + u.key_off;
+  const float* occ = a.occ + u.occ_off + static_cast<size_t>(t) * u.nkey;
+  const bool vec = (A & 3) == 0 && A <= kDenseVec * kDenseThreads * 4;
+  if (gr && vec) {
+    for (int w = tid; w < (A + 31) / 32; w += kDenseThreads) bits[w] = 0u;
+    __syncthreads();
+    for (int j = tid; j < u.nkey; j += kDenseThreads) atomicOr(&bits[keys[j] >> 5], 1u << (keys[j] & 31));
+  }
+  if (vec) {
+    const int n4 = A >> 2;
+    const float4* x4 = reinterpret_cast<const float4*>(xr);
+    float4 v[kDenseVec];
+    float m = -__builtin_huge_valf();
+#pragma unroll
+    for (int j = 0; j < kDenseVec; ++j) {
+      const int q = tid + j * kDenseThreads;
+      v[j] = q < n4 ? ldg_stream(x4 + q) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      m = fmaxf(m, fmaxf(fmaxf(v[j].x, v[j].y), fmaxf(v[j].z, v[j].w)));
+    }
+    m = block_max(m, sh);
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < kDenseVec; ++j) {
+      const int q = tid + j * kDenseThreads;
+      if (q < n4) s += (__expf(v[j].x - m) + __expf(v[j].y - m)) + (__expf(v[j].z - m) + __expf(v[j].w - m));
+    }
+    s = block_sum(s, sh);
+    const float ls = logf(s);
+    if (tid == 0) a.lse[row] = make_float2(m, ls);
+    if (!gr) return;
+    float4* g4 = reinterpret_cast<float4*>(gr);
+#pragma unroll
+    for (int j = 0; j < kDenseVec; ++j) {
+      const int q = tid + j * kDenseThreads;
+      if (q >= n4) continue;
+      float o[4] = {expf((v[j].x - m) - ls), expf((v[j].y - m) - ls), expf((v[j].z - m) - ls),
+                    expf((v[j].w - m) - ls)};
+      const unsigned word = bits[(4 * q) >> 5] >> ((4 * q) & 31);
+      if (word & 0xFu) {
+        for (int e = 0; e < 4; ++e) {
+          if (!((word >> e) & 1u)) continue;
+          const int c = 4 * q + e;
+          for (int j2 = 0; j2 < u.nkey; ++j2)
+            if (keys[j2] == c) o[e] -= occ[j2];
+        }
+      }
+      stg_stream(g4 + q, make_float4(o[0], o[1], o[2], o[3]));
+    }
+  } else {  // generic: two passes (the second hits L1/L2)
+    float m = -__builtin_huge_valf();
+    for (int c = tid; c < A; c += kDenseThreads) m = fmaxf(m, __ldg(xr + c));
+    m = block_max(m, sh);
+    float s = 0.f;
+    for (int c = tid; c < A; c += kDenseThreads) s += __expf(__ldg(xr + c) - m);
+    s = block_sum(s, sh);
+    const float ls = logf(s);
+    if (tid == 0) a.lse[row] = make_float2(m, ls);
+    if (!gr) return;
+    for (int c = tid; c < A; c += kDenseThreads) gr[c] = expf((__ldg(xr + c) - m) - ls);
+    __syncthreads();
+    for (int j = tid; j < u.nkey; j += kDenseThreads) gr[keys[j]] -= occ[j];
+  }
+  (void)nkey_s;
+}
+
+// costs[b] = sum_t lse_t - log Z (natural log), one warp per utterance.
+__global__ void k_finalize(PairArgs a) {
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= a.B) return;
+  const UttDesc u = a.desc[b];
+  if (u.status != 0) {
+    if (lane == 0) a.costs[b] = u.status == 2 ? 0.f : __builtin_huge_valf();
+    return;
+  }
+  const double lz = a.logz[b];
+  double acc = 0.0;
+  for (int t = lane; t < u.T; t += 32) {
+    const float2 v = a.lse[static_cast<size_t>(t) * a.B + b];
+    acc += static_cast<double>(v.x) + static_cast<double>(v.y);
+  }
+  acc = warp_sum_d(acc);
+  if (lane == 0) a.costs[b] = lz == -__builtin_huge_val() ? __builtin_huge_valf() : static_cast<float>(acc - lz * kLn2);
+}
+
+// Trainer scalars (trainer.cpp:160-168): sum of finite costs, count of
+// infeasible ones; one warp, lane-strided then a fixed xor tree.
+__global__ void k_loss_sum(const float* __restrict__ costs, int B, double* __restrict__ out2) {
+  const int lane = threadIdx.x;
+  double loss = 0.0, skipped = 0.0;
+  for (int b = lane; b < B; b += 32) {
+    const float c = costs[b];
+    if (isfinite(c)) loss += static_cast<double>(c);
+    else skipped += 1.0;
+  }
+  loss = warp_sum_d(loss);
+  skipped = warp_sum_d(skipped);
+  if (lane == 0) {
+    out2[0] = loss;
+    out2[1] = skipped;
+  }
+}
+
+}  // namespace
+
+int launch_dense(const PairArgs& a, bool write_grad, void* stream) {
+  const long long rows = static_cast<long long>(a.t_max) * a.B;
+  if (rows == 0) return cudaSuccess;
+  k_dense<<<static_cast<unsigned>(rows), kDenseThreads, 0, static_cast<cudaStream_t>(stream)>>>(a, write_grad ? 1 : 0);
+  return cudaGetLastError();
+}
+
+int launch_finalize(const PairArgs& a, void* stream) {
+  if (a.B == 0) return cudaSuccess;
+  k_finalize<<<(a.B + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  return cudaGetLastError();
+}
+
+int launch_loss_sum(const float* costs, int B, double* out2, void* stream) {
+  k_loss_sum<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(costs, B, out2);
+  return cudaGetLastError();
+}
+
+}  // namespace ds2ctc

@@ -1,48 +1,135 @@
 // ds2ctc_internal.h -- shared host/device definitions of the CTC pipeline.
 //
-// Pipeline per ds2ctc_compute_loss call (all on the caller's stream):
-//   H2D   one packed metadata blob (UttDesc[], launch order, labels, key CSR)
-//   K1    rowstats   : per frame (max, log-sum-exp) of the logits   (HBM-bound)
-//   K2/3  pair chain : per utterance a 2-CTA cluster, alpha forward || beta
-//                      backward, meet at the midpoint, then each CTA fuses
-//                      occupancy + gradient for its half             (latency-bound)
-//   K4    dense      : large alphabets only -- one coalesced pass writing
-//                      softmax - occupancy                             (HBM-bound)
+// Per ds2ctc_compute_loss call (all on the caller's stream):
+//   H2D    one packed metadata blob (UttDesc[], launch order, labels, key CSR)
+//   pair   k_pair: per utterance a 2-CTA cluster, alpha forward || beta
+//          backward over the RAW logits, meeting at frame tm = (T-1)/2; each
+//          CTA then streams its half of gamma = alpha+beta into occupancies.
+//          Small alphabets (A <= kFusedMaxAlphabet): the same kernel also
+//          computes the per-frame log-softmax statistics, the gradient rows
+//          softmax - occupancy and the costs -> ONE launch per call.
+//   dense  large alphabets only: one coalesced pass per frame computing the
+//          log-sum-exp and writing softmax - occupancy (key chars only)
+//   final  large alphabets only: costs = sum_t lse_t - log Z
 #pragma once
 
 #include <cstddef>
 #include <cstdint>
 
+#ifdef __CUDACC__
+#define DS2CTC_HD __host__ __device__
+#else
+#define DS2CTC_HD
+#endif
+
 namespace ds2ctc {
 
-constexpr int kMaxStates = 4095;   // == DS2CTC_MAX_STATES
-constexpr int kFusedMaxAlphabet = 1024;
+constexpr int kMaxStates = 4095;  // == DS2CTC_MAX_STATES
+constexpr int kFusedMaxAlphabet = 128;
+constexpr int kMaxThreads = 320;  // chain warps (<= 8 at K = 8, L <= 2047) + 1 service warp
 constexpr size_t kAlign = 256;
+constexpr size_t kSmemBudget = 220 * 1024;
 
 // Per-utterance descriptor, computed on the host, read by every kernel.
 struct alignas(16) UttDesc {
-  int T;         // input length (frames)
-  int L;         // label length
-  int S;         // 2L+1
-  int status;    // 0 = run, 1 = infeasible (T < min_frames), 2 = trivial (T == 0, L == 0: cost 0)
-  int lab_off;   // offset into labels[]
-  int nkey;      // key slots: slot 0 = blank, slots 1..nkey-1 = distinct non-blank symbols
-  int key_off;   // offset into key_char[] / key_start[] (key_start has nkey+1 entries at key_off+b)
-  int row_off;   // offset into key_rows[] (odd lattice rows grouped by slot)
-  long long store_off;  // offset (doubles) into the half-lattice store: S * (T + 1) doubles
-  long long occ_off;    // offset (floats) into the compact occupancy rows (dense path): T * nkey
-  int tm;        // meet-in-the-middle frame
+  int T;          // input length (frames)
+  int L;          // label length
+  int S;          // 2L+1
+  int status;     // 0 = run, 1 = infeasible (T < min_frames), 2 = trivial (T == 0, L == 0: cost 0)
+  int lab_off;    // offset into labels[] (also into key_pos[])
+  int nkey;       // key slots: slot 0 = blank, slots 1.. = distinct non-blank symbols ascending
+  int key_off;    // offset into key_char[]; key_start has nkey+1 entries at key_off + b
+  int col_w;      // floats per stored lattice column: roundup4(S) + roundup4(chain warps)
+  long long store_off;  // offset (floats) into the half-lattice store: col_w * (T + 1)
+  long long occ_off;    // offset (floats) into the compact occupancy rows (split path): T * nkey
+  int tm;         // meet-in-the-middle frame
   int pad0, pad1, pad2;
 };
 static_assert(sizeof(UttDesc) == 64, "UttDesc layout");
 
+DS2CTC_HD inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+// Launch geometry shared by every utterance of one call.
+struct Geometry {
+  int K;          // label pairs per chain thread
+  int nchain;     // chain warps (max over the batch)
+  int P;          // epoch length (steps between CTA barriers)
+  int SW;         // staged symbols per frame: A (fused) or max nkey (split)
+  int max_L;
+  int fused;
+  // shared-memory carve-up (bytes, 16-aligned)
+  int off_xraw, off_emis, off_lse, off_eb, off_el, off_sring, off_tile, off_occ, off_bnd, off_meta, off_red;
+  int xstride;    // floats per xraw row (odd)
+  int estride;    // floats per eb/el row (odd)
+  int cw_max;     // floats per stored column (max over batch)
+  int tstride;    // floats per tile row (odd)
+  int ostride;    // floats per occ scratch row (odd)
+  int smem;       // total bytes
+};
+
+DS2CTC_HD inline int chain_warps_for(int L, int K) { return (L + 1 + 32 * K - 1) / (32 * K); }
+
+// Label pairs per chain thread. At most three chain warps while K <= 8, so
+// the service warp keeps an SM sub-partition (SMSP) of its own; each pair
+// costs 5 MUFU ops per step, so K also bounds the per-SMSP MUFU load.
+constexpr int kPairChoices[] = {1, 2, 3, 4, 6, 8};
+inline int pick_K(int max_L) {
+  const int pairs = max_L + 1;
+  for (int K : kPairChoices)
+    if (pairs <= 96 * K) return K;
+  return 8;
+}
+
+inline int column_width(int L, int K) { return round_up(2 * L + 1, 4) + round_up(chain_warps_for(L, K), 4); }
+
+inline Geometry make_geometry(int max_L, int max_nkey, int A, bool fused) {
+  Geometry g{};
+  g.K = pick_K(max_L);
+  g.nchain = chain_warps_for(max_L, g.K);
+  g.max_L = max_L;
+  g.fused = fused ? 1 : 0;
+  g.SW = fused ? A : max_nkey;
+  g.cw_max = column_width(max_L, g.K);
+  for (int P = 32; P >= 2; P /= 2) {
+    g.P = P;
+    g.xstride = g.SW | 1;
+    g.estride = (max_L + 1) | 1;
+    g.tstride = (fused ? A : max_nkey) | 1;
+    g.ostride = max_nkey | 1;
+    int off = 0;
+    auto take = [&](int bytes) {
+      int o = off;
+      off += round_up(bytes, 16);
+      return o;
+    };
+    const int RX = 4 * P;
+    g.off_xraw = take(4 * RX * g.xstride);
+    g.off_emis = take(8 * 2 * P * g.SW);
+    g.off_lse = take(8 * RX);
+    g.off_eb = take(4 * 2 * P * g.estride);
+    g.off_el = take(4 * 2 * P * g.estride);
+    g.off_sring = take(4 * 2 * P * g.cw_max);
+    g.off_tile = take(4 * P * g.tstride);
+    g.off_occ = take(4 * P * g.ostride);
+    g.off_bnd = take(8 * g.nchain * 2 * P);
+    // meta: labels (L+1), key_char (nkey), key_start (nkey+1), key_pos (L), slot of each label
+    // position (L+1), symbol -> slot (A shorts, fused)
+    g.off_meta = take(4 * (3 * max_L + 2 * max_nkey + 8) + (fused ? 2 * A : 0));
+    g.off_red = take(8 * 72);
+    g.smem = off;
+    if (static_cast<size_t>(off) <= kSmemBudget) break;
+  }
+  return g;
+}
+
 // Offsets (bytes) of the workspace regions; a pure function of the lengths.
 struct Layout {
-  size_t desc, order, labels, key_char, key_start, key_rows, meta_end;  // metadata blob (int32 words)
-  size_t stats;   // float2 [T_max * B]
-  size_t store;   // double [sum S_b (T_b + 1)]
-  size_t occ;     // float  [sum T_b (L_b + 1)] (dense path only)
+  size_t desc, order, labels, key_char, key_start, key_pos, meta_end;  // metadata blob (int32 words)
+  size_t store;   // float [sum col_w (T_b + 1)]
+  size_t occ;     // float [sum T_b (L_b + 1)]   (split path)
+  size_t lse;     // float2 [T_max * B]          (split path)
   size_t logz;    // double [B]
+  size_t part;    // double [2B] per-CTA partial lse sums (fused path)
   size_t total;
   int t_max;
   long long sum_L;
@@ -53,58 +140,61 @@ inline size_t align_up(size_t v, size_t a = kAlign) { return (v + a - 1) / a * a
 inline Layout make_layout(const int* label_lengths, const int* input_lengths, int A, int B) {
   Layout lay{};
   long long sum_L = 0, store = 0, occ = 0;
-  int t_max = 0;
+  int t_max = 0, max_L = 0;
+  for (int b = 0; b < B; ++b) max_L = label_lengths[b] > max_L ? label_lengths[b] : max_L;
+  const int K = pick_K(max_L);
   for (int b = 0; b < B; ++b) {
     long long L = label_lengths[b], T = input_lengths[b];
     sum_L += L;
-    store += (2 * L + 1) * (T + 1);
+    store += static_cast<long long>(column_width(static_cast<int>(L), K)) * (T + 1);
     occ += T * (L + 1);
     if (T > t_max) t_max = static_cast<int>(T);
   }
+  const bool split = A > kFusedMaxAlphabet;
   size_t off = 0;
   lay.desc = off;      off += sizeof(UttDesc) * B;
   lay.order = off;     off += sizeof(int) * B;
   lay.labels = off;    off += sizeof(int) * sum_L;
   lay.key_char = off;  off += sizeof(int) * (sum_L + B);
   lay.key_start = off; off += sizeof(int) * (sum_L + 2 * B);
-  lay.key_rows = off;  off += sizeof(int) * sum_L;
+  lay.key_pos = off;   off += sizeof(int) * sum_L;
   lay.meta_end = off;
   off = align_up(off);
-  lay.stats = off;     off = align_up(off + sizeof(float) * 2 * static_cast<size_t>(t_max) * B);
-  lay.store = off;     off = align_up(off + sizeof(double) * static_cast<size_t>(store));
-  lay.occ = off;
-  if (A > kFusedMaxAlphabet) off += sizeof(float) * static_cast<size_t>(occ);
-  off = align_up(off);
+  lay.store = off;     off = align_up(off + sizeof(float) * static_cast<size_t>(store));
+  lay.occ = off;       if (split) off = align_up(off + sizeof(float) * static_cast<size_t>(occ));
+  lay.lse = off;       if (split) off = align_up(off + sizeof(float) * 2 * static_cast<size_t>(t_max) * B);
   lay.logz = off;      off = align_up(off + sizeof(double) * B);
+  lay.part = off;      off = align_up(off + sizeof(double) * 2 * B);
   lay.total = off;
   lay.t_max = t_max;
   lay.sum_L = sum_L;
   return lay;
 }
 
-// Kernel launch parameters (device pointers into the caller's buffers/workspace).
-struct ChainArgs {
+// Kernel arguments (device pointers into the caller's buffers / workspace).
+struct PairArgs {
   const float* x;        // [T_max][B][A]
-  float* grad;           // [T_max][B][A] or nullptr
+  float* grad;           // [T_max][B][A] or nullptr (cost only)
   float* costs;          // [B]
   const UttDesc* desc;
   const int* order;
   const int* labels;
   const int* key_char;
   const int* key_start;
-  const int* key_rows;
-  const float2* stats;   // [T_max][B]
-  double* store;
-  float* occ;            // dense path compact occupancy rows, nullptr when fused
-  double* logz;          // [B] log2-domain log Z (-inf when infeasible)
+  const int* key_pos;
+  float* store;          // half-lattice columns
+  float* occ;            // split path: compact occupancy rows
+  float2* lse;           // split path: per-frame (max, log-sum-exp)
+  double* logz;          // [B] log2-domain log Z (-inf when the lattice has zero mass)
+  double* part;          // [2B] per-CTA partial sums of lse (fused path)
   int t_max, B, A, blank;
-  int nthreads;          // CTA size of the chain kernel
-  int cells;             // cells per thread (K)
+  Geometry g;
 };
 
-// Launchers (ctc_kernels.cu). Return cudaError_t as int.
-int launch_rowstats(const ChainArgs& a, void* stream);
-int launch_chain(const ChainArgs& a, void* stream);
-int launch_dense(const ChainArgs& a, void* stream);
+// Launchers (ctc_pair.cu / ctc_dense.cu). Return cudaError_t as int.
+int launch_pair(const PairArgs& a, void* stream);
+int launch_dense(const PairArgs& a, bool write_grad, void* stream);
+int launch_finalize(const PairArgs& a, void* stream);
+int launch_loss_sum(const float* costs, int B, double* out2, void* stream);
 
 }  // namespace ds2ctc

@@ -40,10 +40,10 @@ def test_workspace_size_monotone():
     b = ctc.workspace_size([150] * 64, [700] * 64, 29)
     c = ctc.workspace_size([60] * 64, [350] * 64, 6000)
     assert 0 < a < b
-    # half-lattice store alone: sum S*(T+1) doubles
-    assert b >= 64 * 301 * 701 * 8
-    # the dense path also keeps compact occupancy rows
-    assert c >= 64 * 121 * 351 * 8 + 64 * 350 * 61 * 4
+    # half-lattice store: per frame fp32 deltas (2L+1 -> mult. of 4) + per-warp offsets
+    assert b >= 64 * (304 + 4) * 701 * 4
+    # the split (large-alphabet) path also keeps compact occupancy rows and per-frame lse
+    assert c >= 64 * (124 + 4) * 351 * 4 + 64 * 350 * 61 * 4 + 64 * 350 * 8
     assert ctc.workspace_size([], [], 29) == 0
 
 

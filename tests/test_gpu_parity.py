@@ -28,6 +28,9 @@ def run_gpu(acts, flat, ll, il, blank=None, want_grad=True):
     return costs.cpu().numpy().astype(np.float64), (grads.cpu().numpy() if grads is not None else None)
 
 
+ERRORS = {}
+
+
 def assert_parity(costs, grads, ref_costs, ref_grads, il, what):
     inf_ref = ~np.isfinite(ref_costs)
     assert np.array_equal(~np.isfinite(costs), inf_ref), f"{what}: infeasible set differs {costs} {ref_costs}"
@@ -41,6 +44,11 @@ def assert_parity(costs, grads, ref_costs, ref_grads, il, what):
         assert ok.all(), f"{what}: cost rel err {rel.max():.3e}"
     if grads is not None:
         err = np.abs(grads.astype(np.float64) - ref_grads.astype(np.float64))
+        if fin.any():
+            rel_max = float((np.abs(costs[fin] - ref_costs[fin]) / np.maximum(np.abs(ref_costs[fin]), 1e-30)).max())
+        else:
+            rel_max = 0.0
+        print(f"PARITY {what}: max rel cost err {rel_max:.3e}, max abs grad err {err.max():.3e}")
         assert err.max() <= GRAD_ATOL, f"{what}: grad abs err {err.max():.3e}"
         for b in np.where(inf_ref)[0]:
             assert np.all(grads[:, b, :] == 0), f"{what}: infeasible utterance {b} has nonzero gradient"
@@ -68,6 +76,11 @@ def test_cost_only_matches(golden, cuda):
     assert grads is None
     ref = golden[f"{name}/costs"]
     assert np.max(np.abs(costs - ref) / np.abs(ref)) <= COST_RTOL
+    # large-alphabet cost-only path (k_pair + lse pass + finalize)
+    acts, flat, ll, il = fixed_shape_batch(6000, 120, 30, 3, seed=8)
+    costs, grads = run_gpu(acts, flat, ll, il, want_grad=False)
+    rc, _ = oracle.oracle_batch(acts, flat, ll, il, want_grad=False)
+    assert grads is None and np.max(np.abs(costs - rc) / np.abs(rc)) <= COST_RTOL
 
 
 @pytest.mark.parametrize("shape", [("english", 29, 700, 150, 64), ("mandarin", 6000, 350, 60, 6)])
@@ -92,6 +105,16 @@ def test_sortagrad_variable_vs_oracle(cuda):
     costs, grads = run_gpu(acts, flat, ll, il)
     rc, rg = oracle.oracle_batch(acts, flat, ll, il, nthreads=8)
     assert_parity(costs, grads, rc, rg, il, "sortagrad")
+
+
+@pytest.mark.parametrize("A,T,L,B", [(29, 1300, 600, 2), (29, 2100, 1000, 2), (200, 300, 90, 4), (5, 40, 15, 33)])
+def test_geometry_variants_vs_oracle(cuda, A, T, L, B):
+    # 1024-thread CTA (L+1 > 480), two label pairs per thread (L+1 > 992),
+    # split path just above the fused alphabet limit, and an odd batch with A=5
+    acts, flat, ll, il = fixed_shape_batch(A, T, L, B, seed=17)
+    costs, grads = run_gpu(acts, flat, ll, il)
+    rc, rg = oracle.oracle_batch(acts, flat, ll, il, nthreads=8)
+    assert_parity(costs, grads, rc, rg, il, f"A{A}T{T}L{L}")
 
 
 def test_gradient_rows_sum_to_zero_full_size(cuda):

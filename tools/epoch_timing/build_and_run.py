@@ -1,0 +1,84 @@
+"""Debug-only: build libds2ctc with -DDS2CTC_EPOCH_TIMING and print per-epoch
+warp busy cycles of the first cluster for one workload (design evidence)."""
+import ctypes
+import os
+import subprocess
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+CSRC = os.path.join(ROOT, "paper_1512_02595_b200", "csrc")
+OUT = os.path.join(ROOT, "build", "epoch_timing")
+
+
+def build(defines=()):
+    os.makedirs(OUT, exist_ok=True)
+    tag = "_".join(d.lower() for d in defines) or "base"
+    so = os.path.join(OUT, f"libds2ctc_timing_{tag}.so")
+    objs = []
+    for src in ("ctc_pair.cu", "ctc_dense.cu"):
+        obj = os.path.join(OUT, tag + src + ".o")
+        subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo",
+                        "-DDS2CTC_EPOCH_TIMING", *[f"-DDS2CTC_EXP_{d}" for d in defines], "-Xcompiler", "-fPIC", f"-I{ROOT}/include", f"-I{CSRC}", "-c",
+                        os.path.join(CSRC, src), "-o", obj], check=True)
+        objs.append(obj)
+    for src in ("ctc_api.cpp", "scheduler.cpp"):
+        obj = os.path.join(OUT, src + ".o")
+        subprocess.run(["g++", "-O2", "-std=c++17", "-fPIC", f"-I{ROOT}/include", f"-I{CSRC}",
+                        "-I/usr/local/cuda/include", "-c", os.path.join(CSRC, src), "-o", obj], check=True)
+        objs.append(obj)
+    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", so,
+                    *objs], check=True)
+    return so
+
+
+def run(so, A=29, T=700, L=150, B=64, brief=False):
+    import torch
+
+    from paper_1512_02595_b200 import _lib
+    from paper_1512_02595_b200.synth import fixed_shape_batch
+
+    _lib.LIB_PATH = so
+    _lib._lib = None
+    from paper_1512_02595_b200 import ctc
+
+    acts, flat, ll, il = fixed_shape_batch(A, T, L, B)
+    x = torch.from_numpy(acts).cuda()
+    for _ in range(3):
+        ctc.compute_ctc_loss(x, flat, ll, il)
+    torch.cuda.synchronize()
+    buf = np.zeros((2, 128, 33, 2), dtype=np.int64)
+    lib = ctypes.CDLL(so)
+    assert lib.ds2ctc_debug_epoch_clocks(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong))) == 0
+    if brief:
+        for cta in range(2):
+            rows = [buf[cta, e] for e in range(128) if buf[cta, e, 0, 0] != 0]
+            p1 = [r for r in rows[:8]]
+            busy = np.mean([[int(r[w, 1] - r[w, 0]) for w in range(4)] for r in p1], axis=0)
+            total = int(rows[-1][0, 1] - rows[0][0, 0])
+            print(f"  cta{cta}: total {total} cycles, phase-1 epoch busy per warp {busy.astype(int).tolist()}")
+        return
+    for cta in range(2):
+        e0 = buf[cta, 0, 0, 0]
+        print(f"CTA {cta} ({'fwd' if cta == 0 else 'bwd'})")
+        for e in range(128):
+            row = buf[cta, e]
+            if row[0, 0] == 0:
+                break
+            busy = [int(row[w, 1] - row[w, 0]) for w in range(33) if row[w, 0] > 0]
+            start = int(row[0, 0] - e0)
+            print(f"  epoch {e:3d} start {start:8d}  busy per warp {busy}")
+
+
+if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "variants":
+        for defs in [(), ("NOSTORE",), ("NOREDUX",), ("NOEMIS",), ("NOSTORE", "NOEMIS")]:
+            so = build(defs)
+            print("variant", defs or "base")
+            run(so, brief=True)
+    else:
+        so = build()
+        args = [int(v) for v in sys.argv[1:]]
+        run(so, *args)
