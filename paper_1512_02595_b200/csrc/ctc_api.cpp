@@ -240,7 +240,9 @@ ds2ctc_status run(const float* acts, float* grads, const int* flat_labels, const
   a.B = B;
   a.A = A;
   a.blank = blank;
-  a.g = make_geometry(mx.first, mx.second, A, fused);
+  int max_L_all = 0;
+  for (int b = 0; b < B; ++b) max_L_all = std::max(max_L_all, label_lengths[b]);
+  a.g = make_geometry(max_L_all, mx.first, mx.second, A, fused);
   if (static_cast<size_t>(a.g.smem) > kSmemBudget) return DS2CTC_STATUS_UNSUPPORTED;
 
   int dev = 0;

@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense(PairArgs a, int write_g
 }
 
 // costs[b] = sum_t lse_t - log Z (natural log), one warp per utterance.
+// log Z = log Z' + sum_t mk_t, with log Z' (log2 units) from k_pair.
 __global__ void k_finalize(PairArgs a) {
   const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -173,7 +174,11 @@ __global__ void k_finalize(PairArgs a) {
     acc += static_cast<double>(v.x) + static_cast<double>(v.y);
   }
   acc = warp_sum_d(acc);
-  if (lane == 0) a.costs[b] = lz == -__builtin_huge_val() ? __builtin_huge_valf() : static_cast<float>(acc - lz * kLn2);
+  // k_pair ran on frames shifted by mk_t and left -sum_t mk_t in part[2b], part[2b+1].
+  if (lane == 0)
+    a.costs[b] = lz == -__builtin_huge_val()
+                     ? __builtin_huge_valf()
+                     : static_cast<float>((acc + (a.part[2 * b] + a.part[2 * b + 1])) - lz * kLn2);
 }
 
 // Trainer scalars (trainer.cpp:160-168): sum of finite costs, count of

@@ -14,21 +14,30 @@
 // streams its second half into occupancies gamma = alpha + beta - log Z,
 // reading the partner's stored half. The serial chain is T steps, not 2T.
 //
-// Numerics: the recursion runs on the RAW logits in
-// log2 units (per-frame normalisation cancels in gamma, and log p = log Z -
-// sum_t lse_t); carried values are double-float (hi, lo fp32) so rounding does
-// not accumulate as ulp(|alpha|) per step; the log-sum-exp correction uses
-// MUFU ex2/lg2. Stored half-lattice cells are fp32 deltas from a per-warp max.
+// Numerics:
+//  * log2 units; each frame is shifted by mk_t = max over the staged symbols
+//    (the shift cancels in gamma; the cost adds it back), and the shifted
+//    emission (x - mk_t) * log2(e) is formed exactly as a double-float.
+//  * the carried lattice value is a double-float (hi, lo fp32), so rounding
+//    does not accumulate as ulp(|alpha|) per step; the log-sum-exp
+//    correction uses MUFU ex2/lg2 on the (small) differences only.
+//  * -inf is represented by a large negative sentinel (-1e30), so the
+//    recursion has no NaN paths and no -inf guards; anything below -1e29 is
+//    -inf when stored or combined.
+//  * stored half-lattice cells are fp32 deltas from a per-warp max.
 //
-// Thread layout. Chain thread i owns label pairs i*K .. i*K+K-1. In the
-// forward CTA pair j is (blank 2j, label 2j+1); in the backward CTA it is
-// (label 2j-1, blank 2j). Either way a pair needs exactly ONE value from the
-// neighbouring pair per step, which arrives by warp shuffle, or, across warp
-// boundaries, through a tagged shared-memory ring (no CTA barrier per step).
-// A service warp stages logits (cp.async) and the partner's columns, computes
-// the per-frame log-softmax statistics, and turns occupancy rows into
-// gradient rows (softmax - occupancy, ctc.cpp:69-79) one epoch behind the
-// chain. All warps meet at a CTA barrier every P steps (an epoch).
+// Warp roles. Chain thread i owns label pairs i*K .. i*K+K-1 (forward pair j
+// = (blank 2j, label 2j+1); backward pair j = (label 2j-1, blank 2j)), so a
+// pair needs ONE value from its neighbour per step: a warp shuffle, or,
+// across warps, a tagged shared-memory ring (no CTA barrier per step). Chain
+// warps do only the recursion and publish each column to a tagged ring; a
+// helper warp per chain warp (same lanes, same cells) turns published
+// columns into stored deltas (phase 1) or occupancies (phase 2) using the
+// SM sub-partition issue slots the latency-bound chain leaves idle. A
+// service warp stages logits (cp.async) and the partner's columns, computes
+// the per-frame statistics and emissions, and turns occupancy rows into
+// gradient rows (softmax - occupancy, ctc.cpp:69-79) one epoch behind. All
+// warps meet at a CTA barrier every P steps (an epoch).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -43,12 +52,14 @@ constexpr float kL2eL = 1.925963033500011e-08f;      // log2 e - kL2eH
 constexpr float kLn2f = 0.693147180559945309f;
 constexpr double kLn2 = 0.69314718055994530942;
 constexpr float NEGF = -__builtin_huge_valf();
+constexpr float SENT = -1e30f;     // "-inf" inside the recursion
+constexpr float SENT_CUT = -1e29f;  // below this a value is -inf
 
 struct DF {
   float h, l;
 };
 
-__device__ __forceinline__ DF dneg() { return {NEGF, 0.f}; }
+__device__ __forceinline__ DF sent() { return {SENT, 0.f}; }
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -68,54 +79,45 @@ __device__ __forceinline__ DF two_sum(float a, float b) {
   return {s, (a - (s - bb)) + (b - bb)};
 }
 
-__device__ __forceinline__ DF fast2(float a, float b) {
-  const float s = a + b;
-  return {s, b - (s - a)};
+// (x - mk) * log2(e) as an exact-to-fp32^2 double-float; -inf -> sentinel.
+__device__ __forceinline__ float2 emis_df(float x, float mk) {
+  const DF d = two_sum(x, -mk);
+  const float h = d.h * kL2eH;
+  const float l = fmaf(d.h, kL2eH, -h) + (d.h * kL2eL + d.l * kL2eH);
+  return x == NEGF ? make_float2(SENT, 0.f) : make_float2(h, l);
 }
 
-// x * log2(e) as a double-float (x is exact in fp32).
-__device__ __forceinline__ float2 emis_df(float x) {
-  const float h = x * kL2eH;
-  const float l = fmaf(x, kL2eH, -h) + x * kL2eL;
-  return x == NEGF ? make_float2(NEGF, 0.f) : make_float2(h, l);
+// Sorted log-sum-exp (log_sum_exp_guarded, ctc.hpp:30-35, in log2 units):
+// result = base + c with base the largest operand (exact double-float) and
+// c = lg2(1 + sum 2^(other - base)), the differences taken as double-floats.
+__device__ __forceinline__ float lse2(DF a, DF b, DF& base) {
+  const float d = (a.h - b.h) + (a.l - b.l);
+  base = d >= 0.f ? a : b;
+  return lg2(1.f + ex2(-fabsf(d)));
 }
 
-// Sorted log-sum-exp: the largest operand (by hi part) is kept exactly as the
-// double-float base and only the others go through MUFU ex2, so a 2-way LSE
-// costs ex2 + lg2 and a 3-way one 2 ex2 + lg2 (log_sum_exp_guarded,
-// ctc.hpp:30-35: -inf operands contribute 0). Result = base + c.
-struct LSE {
-  DF base;
-  float c;
-};
-
-__device__ __forceinline__ LSE lse2(DF a, DF b) {
-  const bool p = a.h >= b.h;
-  const DF hi = p ? a : b, lo = p ? b : a;
-  const float d = (lo.h - hi.h) + (lo.l - hi.l);
-  return {hi, lg2(1.f + ex2(d))};
+__device__ __forceinline__ float lse3(DF a, DF b, DF c, DF& base) {
+  const float d1 = (a.h - b.h) + (a.l - b.l);
+  const DF hi = d1 >= 0.f ? a : b;
+  const float d2 = (hi.h - c.h) + (hi.l - c.l);
+  base = d2 >= 0.f ? hi : c;
+  return lg2((1.f + ex2(fminf(d2, 0.f) - fabsf(d1))) + ex2(-fabsf(d2)));
 }
 
-__device__ __forceinline__ LSE lse3(DF a, DF b, DF c) {
-  const bool p = a.h >= b.h;
-  const DF hi = p ? a : b, lo = p ? b : a;
-  const bool q = hi.h >= c.h;
-  const DF m = q ? hi : c, o = q ? c : hi;
-  const float d1 = (lo.h - m.h) + (lo.l - m.l);
-  const float d2 = (o.h - m.h) + (o.l - m.l);
-  return {m, lg2((1.f + ex2(d1)) + ex2(d2))};
+// base + c + e, renormalised (Fast2Sum: |base| >= |e| except within the
+// first few frames, where both are small).
+__device__ __forceinline__ DF incl(DF m, float c, float2 e) {
+  const float s = m.h + e.x;
+  const float err = e.x - (s - m.h);
+  const float lo = ((m.l + e.y) + err) + c;
+  const float h = s + lo;
+  return {h, lo - (h - s)};
 }
 
-// base + c + emission, with the reference guard `acc == -inf ? -inf : acc + lp` (ctc.cpp:231).
-__device__ __forceinline__ DF incl(LSE m, float2 e) {
-  const DF s = two_sum(m.base.h, e.x);
-  const DF r = fast2(s.h, ((s.l + m.base.l) + e.y) + m.c);
-  return (m.base.h == NEGF || e.x == NEGF) ? dneg() : r;
-}
-
-__device__ __forceinline__ DF excl(LSE m) {
-  const DF r = fast2(m.base.h, m.base.l + m.c);
-  return m.base.h == NEGF ? dneg() : r;
+__device__ __forceinline__ DF excl(DF m, float c) {
+  const float lo = m.l + c;
+  const float h = m.h + lo;
+  return {h, lo - (h - m.h)};
 }
 
 __device__ __forceinline__ void cluster_barrier() {
@@ -149,32 +151,65 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-// Tagged warp-boundary handoff: (hi, lo) with the step's low 8 bits in the
-// lo mantissa (a 2^-16 relative perturbation of lo, i.e. ~2^-40 of the value).
-// Predicated store (no branch, so no reconvergence point on the critical path).
-__device__ __forceinline__ void bnd_put(bool pred, unsigned long long* slot, DF v, int tag) {
+// Tagged values: (hi, lo) with the step's low 8 bits in the lo mantissa (a
+// 2^-16 relative perturbation of lo, i.e. ~2^-40 of the value). An aligned
+// 64-bit shared store is single-copy atomic, so a reader that sees the tag
+// sees the value.
+__device__ __forceinline__ unsigned long long tag_pack(DF v, int tag) {
   const unsigned lo = (__float_as_uint(v.l) & ~0xFFu) | (static_cast<unsigned>(tag) & 0xFFu);
-  const unsigned long long u = (static_cast<unsigned long long>(__float_as_uint(v.h)) << 32) | lo;
+  return (static_cast<unsigned long long>(__float_as_uint(v.h)) << 32) | lo;
+}
+
+__device__ __forceinline__ DF tag_unpack(unsigned long long u) {
+  return {__uint_as_float(static_cast<unsigned>(u >> 32)), __uint_as_float(static_cast<unsigned>(u) & ~0xFFu)};
+}
+
+__device__ __forceinline__ void st_tagged(bool pred, unsigned long long* slot, DF v, int tag) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.volatile.shared.u64 [%0], %1;\n\t}" ::"r"(
           smem_addr(slot)),
-      "l"(u), "r"(static_cast<unsigned>(pred)));
+      "l"(tag_pack(v, tag)), "r"(static_cast<unsigned>(pred)));
 }
 
-// Warp-uniform poll: every lane reads the same slot (a broadcast), so the
-// spin loop never diverges; the caller keeps the value for one lane only.
-__device__ __forceinline__ DF bnd_get(const unsigned long long* slot, int tag) {
+// Spin until the slot carries `tag`. Called warp-uniformly where possible.
+// Polls off the critical path back off with nanosleep so that spinning warps
+// do not crowd the shared-memory/shuffle (MIO) queue the recursion uses.
+template <bool kBackoff = false>
+__device__ __forceinline__ DF ld_tagged(const unsigned long long* slot, int tag) {
   unsigned long long u;
-  do {
+  for (;;) {
     asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(u) : "r"(smem_addr(slot)));
-  } while ((u & 0xFFull) != (static_cast<unsigned long long>(tag) & 0xFFull));
-  return {__uint_as_float(static_cast<unsigned>(u >> 32)), __uint_as_float(static_cast<unsigned>(u) & ~0xFFu)};
+    if ((u & 0xFFull) == (static_cast<unsigned long long>(tag) & 0xFFull)) break;
+    if (kBackoff) __nanosleep(32);
+  }
+  return tag_unpack(u);
+}
+
+__device__ __forceinline__ int ld_volatile_int(const int* p) {
+  int v;
+  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)));
+  return v;
+}
+
+__device__ __forceinline__ void st_volatile_int(int* p, int v) {
+  asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v));
 }
 
 #ifdef DS2CTC_EPOCH_TIMING
 // Debug build only (tools/epoch_timing): per-epoch clock64 of every warp of the
 // first cluster, [cta][epoch][warp][start, end].
 __device__ long long g_epoch_clock[2][128][33][2];
+// per-step stamps of epoch 1 for warps 0..7 (lane 0): [cta][warp][step][point]
+__device__ long long g_step_clock[2][8][32][4];
+#define STEP_STAMP(k, e, pt)                                                                            \
+  do {                                                                                                  \
+    if (blockIdx.x < 2 && lane == 0 && warp < 8 && (e).k0 == P && (k) - (e).k0 < 32)                   \
+      g_step_clock[dir][warp][(k) - (e).k0][pt] = clock64();                                            \
+  } while (0)
+#else
+#define STEP_STAMP(k, e, pt) \
+  do {                       \
+  } while (0)
 #endif
 
 // One epoch: steps [k0, k1) of a phase.
@@ -182,8 +217,15 @@ struct Epoch {
   int k0, k1, phase;  // phase 0 = none
 };
 
+// K <= 4 keeps at most three chain warps (7 warps per CTA, full register file);
+// K = 6, 8 (labels longer than 384) may use up to eight.
 template <int K>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMaxThreads, 1) k_pair(PairArgs a) {
+constexpr int max_threads_for() {
+  return K <= 4 ? 32 * 7 : kMaxThreads;
+}
+
+template <int K>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(max_threads_for<K>(), 1) k_pair(PairArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const Geometry& g = a.g;
   const int dir = static_cast<int>(cluster_rank());  // 0: alpha forward, 1: beta backward
@@ -208,6 +250,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMaxThreads, 1) k_pa
   if (u.status != 0) {  // infeasible (ctc.cpp:173) or T == 0 with an empty label
     if (dir == 0 && tid == 0) {
       a.logz[b] = u.status == 2 ? 0.0 : -__builtin_huge_val();
+      a.part[2 * b] = a.part[2 * b + 1] = 0.0;
       if (fused) a.costs[b] = u.status == 2 ? 0.f : __builtin_huge_valf();
     }
     if (fused && want_grad) zero_rows(dir == 0 ? 0 : a.t_max / 2, dir == 0 ? a.t_max / 2 : a.t_max);
@@ -217,24 +260,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMaxThreads, 1) k_pa
   const int T = u.T, L = u.L, S = u.S, tm = u.tm;
   const int P = g.P, RX = 4 * P, P2 = 2 * P;  // powers of two
   const int MX = RX - 1, M2 = P2 - 1;
-  const int S4 = round_up(S, 4);
+  const int RH = g.RH, MH = g.RH - 1;  // power of two
+  const int OB = column_offsets_base(L, K);  // per-thread offsets of a stored column start here
   const int cw = u.col_w;
   const int nw_u = chain_warps_for(L, K);  // chain warps this utterance uses
-  const int SW = g.SW;
+  const int SW = g.SW + 1;  // emission row: staged symbols + the sentinel column g.SW
   const int nstage = fused ? a.A : u.nkey;
   const int kmid = dir == 0 ? tm : T - 1 - tm;
-  const int k2s = dir == 0 ? kmid : kmid + 1;  // first phase-2 step (gradient rows)
-  const int kcount = dir == 0 ? kmid : kmid - 1;  // steps whose frame this CTA adds to sum lse
+  const int k2s = dir == 0 ? kmid : kmid + 1;     // first phase-2 step (gradient rows)
+  const int kcount = dir == 0 ? kmid : kmid - 1;  // steps whose frame this CTA adds to the cost
 
   float* xraw = reinterpret_cast<float*>(smem + g.off_xraw);
   float2* emis = reinterpret_cast<float2*>(smem + g.off_emis);
   float2* lser = reinterpret_cast<float2*>(smem + g.off_lse);
   float* eb = reinterpret_cast<float*>(smem + g.off_eb);
   float* el = reinterpret_cast<float*>(smem + g.off_el);
-  float* sring = reinterpret_cast<float*>(smem + g.off_sring);
   float* tile = reinterpret_cast<float*>(smem + g.off_tile);
   float* occs = reinterpret_cast<float*>(smem + g.off_occ);
   unsigned long long* bnd = reinterpret_cast<unsigned long long*>(smem + g.off_bnd);
+  unsigned long long* hring = reinterpret_cast<unsigned long long*>(smem + g.off_hring);
+  int* hprog = reinterpret_cast<int*>(smem + g.off_hprog);
   int* s_lab = reinterpret_cast<int*>(smem + g.off_meta);
   int* s_kchar = s_lab + (L + 1);
   int* s_kstart = s_kchar + u.nkey;
@@ -251,6 +296,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMaxThreads, 1) k_pa
   if (fused)
     for (int c = tid; c < a.A; c += NT) s_slot[c] = -1;
   for (int q = tid; q < NCW * P2; q += NT) bnd[q] = ~0ull;
+  for (int q = tid; q < NCW * RH * 64 * K; q += NT) hring[q] = ~0ull;
+  for (int q = tid; q < 32; q += NT) hprog[q] = -1;
   __syncthreads();
   if (fused)
     for (int j = tid; j < u.nkey; j += NT) s_slot[s_kchar[j]] = static_cast<short>(j);
@@ -269,81 +316,74 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMaxThreads, 1) k_pa
     return {0, 0, 0};
   };
 
-  // ---- per-thread chain state ----
+  // ---- roles ----
   const bool is_chain = warp < nw_u;
-  const bool service = warp == NCW;
-  const int sidx_b = fused ? a.blank : 0;  // staged index of the blank symbol
-  int sidx_l[K];                           // staged index of each pair's label symbol
-  bool skip[K];                            // skip_allowed(2i+1) (ctc.cpp:41-43)
+  const bool is_helper = warp >= NCW && warp - NCW < nw_u;
+  const bool service = warp == 2 * NCW;
+  const int cwarp = is_helper ? warp - NCW : warp;  // the chain warp whose cells this warp owns
+  const int ctid = cwarp * 32 + lane;               // chain thread index of those cells
+
+  // Cells of this lane (chain and helper share the map).
   bool has_b[K], has_l[K];
 #pragma unroll
   for (int p = 0; p < K; ++p) {
-    const int i = tid * K + p;
-    has_b[p] = is_chain && i <= L;
+    const int i = ctid * K + p;
     const int li = dir == 0 ? i : i - 1;  // label index of this pair's label cell
-    has_l[p] = is_chain && li >= 0 && li < L;
-    const int sym = has_l[p] ? s_lab[li] : a.blank;
-    sidx_l[p] = fused ? sym : (has_l[p] ? s_slotpos[li] : 0);
-    skip[p] = is_chain && i >= 1 && i < L && s_lab[i] != a.blank && s_lab[i] != s_lab[i - 1];
+    has_b[p] = (is_chain || is_helper) && i <= L;
+    has_l[p] = (is_chain || is_helper) && li >= 0 && li < L;
   }
-  DF vb[K], vl[K];  // published values: alpha (forward) or emission-inclusive beta~ (backward)
-  DF xb[K], xl[K];  // backward only: emission-exclusive beta (storage / occupancy)
-  DF qb[K], ql[K];  // the previous column's stored/occupancy values (aux work runs one step behind)
-  float pwb[K], pdb[K], pwl[K], pdl[K];  // partner (woff, delta) of the row the aux step consumes
-  float nwb[K], ndb[K], nwl[K], ndl[K];  // ... prefetched for the next row
-#pragma unroll
-  for (int p = 0; p < K; ++p) {
-    vb[p] = vl[p] = xb[p] = xl[p] = qb[p] = ql[p] = dneg();
-    pwb[p] = pdb[p] = pwl[p] = pdl[p] = nwb[p] = ndb[p] = nwl[p] = ndl[p] = NEGF;
-  }
-  float2 eBp[K], eL[K];  // emissions of the next column (blank, label) per pair
-#pragma unroll
-  for (int p = 0; p < K; ++p) eBp[p] = eL[p] = make_float2(0.f, 0.f);
-  float wprev = NEGF;  // warp max of the previous column (CREDUX issued one step earlier)
+
   float Zh = 0.f, Zl = 0.f;
   double logz2 = 0.0;
-  double lse_acc = 0.0;  // service warp lanes: sum of counted lse (natural log)
+  double part_acc = 0.0;  // service warp lanes: fused sum ls_t, split -sum mk_t (counted frames)
 
-  // ---- service warp: staging / conversion / statistics ----
-  auto stage = [&](const Epoch& e, bool partner) {
+  // =====================================================================
+  // Service warp: staging / emissions / statistics / gradient rows.
+  // =====================================================================
+  auto stage = [&](const Epoch& e) {
     if (e.phase == 0) return;
     for (int k = e.k0; k < e.k1; ++k) {
       const float* src = a.x + static_cast<size_t>(frame(k)) * rs + static_cast<size_t>(b) * a.A;
       float* dst = xraw + (k & MX) * g.xstride;
       for (int c = lane; c < nstage; c += 32) cp_async4(dst + c, src + (fused ? c : s_kchar[c]));
-      if (partner && e.phase == 2) {
-        const float* col = a.store + u.store_off + static_cast<size_t>(frame(k)) * cw;
-        float* sdst = sring + (k & M2) * g.cw_max;
-        for (int c4 = lane; c4 < cw / 4; c4 += 32) cp_async16(sdst + 4 * c4, col + 4 * c4);
-      }
     }
     cp_async_commit();
   };
-  auto convert = [&](const Epoch& e) {  // after the staged data landed (wait + __syncwarp)
+  // After the staged rows landed: per-frame shift mk_t (max over the staged
+  // symbols), log-sum-exp (fused), and the shifted double-float emissions.
+  auto convert = [&](const Epoch& e) {
     if (e.phase == 0) return;
     const int n = e.k1 - e.k0;
-    for (int k = e.k0; k < e.k1; ++k)
-      for (int c = lane; c < nstage; c += 32) emis[(k & M2) * SW + c] = emis_df(xraw[(k & MX) * g.xstride + c]);
-    if (fused && lane < n) {  // per-frame (max, log sum exp), lane = frame (ctc.cpp:24-37)
+    if (lane < n) {  // lane = frame
       const int k = e.k0 + lane;
       const float* xr = xraw + (k & MX) * g.xstride;
       float m0 = NEGF, m1 = NEGF;
       int c = 0;
-      for (; c + 1 < a.A; c += 2) {
+      for (; c + 1 < nstage; c += 2) {
         m0 = fmaxf(m0, xr[c]);
         m1 = fmaxf(m1, xr[c + 1]);
       }
-      if (c < a.A) m0 = fmaxf(m0, xr[c]);
-      const float m = fmaxf(m0, m1);
-      float s0 = 0.f, s1 = 0.f;
-      for (c = 0; c + 1 < a.A; c += 2) {
-        s0 += ex2((xr[c] - m) * kL2eH);
-        s1 += ex2((xr[c + 1] - m) * kL2eH);
+      if (c < nstage) m0 = fmaxf(m0, xr[c]);
+      float mk = fmaxf(m0, m1);
+      if (mk == NEGF) mk = 0.f;  // every staged symbol impossible: any shift works
+      float ls = 0.f;
+      if (fused) {  // log_softmax_rows statistics (ctc.cpp:24-37)
+        float s0 = 0.f, s1 = 0.f;
+        for (c = 0; c + 1 < a.A; c += 2) {
+          s0 += ex2((xr[c] - mk) * kL2eH);
+          s1 += ex2((xr[c + 1] - mk) * kL2eH);
+        }
+        if (c < a.A) s0 += ex2((xr[c] - mk) * kL2eH);
+        ls = lg2(s0 + s1) * kLn2f;
       }
-      if (c < a.A) s0 += ex2((xr[c] - m) * kL2eH);
-      const float ls = lg2(s0 + s1) * kLn2f;
-      lser[k & MX] = make_float2(m, ls);
-      if (k <= kcount) lse_acc += static_cast<double>(m) + static_cast<double>(ls);
+      lser[k & MX] = make_float2(mk, ls);
+      if (k <= kcount) part_acc += fused ? static_cast<double>(ls) : -static_cast<double>(mk);
+    }
+    __syncwarp();
+    for (int k = e.k0; k < e.k1; ++k) {
+      const float mk = lser[k & MX].x;
+      for (int c = lane; c < nstage; c += 32) emis[(k & M2) * SW + c] = emis_df(xraw[(k & MX) * g.xstride + c], mk);
+      if (lane == 0) emis[(k & M2) * SW + g.SW] = make_float2(SENT, 0.f);
     }
   };
   // Gradient rows of a finished phase-2 epoch, lane = row (ctc.cpp:196-203, 69-79).
@@ -405,207 +445,297 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMaxThreads, 1) k_pa
     __syncwarp();
   };
 
-  // ---- chain: critical part of step k (one lattice column) ----
-  // Cells that do not exist get a -inf emission, which makes incl() return
-  // -inf without a predicate on the critical path.
+  // =====================================================================
+  // Chain warps: the recursion only.
+  // =====================================================================
+  // Emission-row index of each cell; cells that do not exist read the
+  // sentinel column (no predicate between the loads and their use).
+  int sidx_b[K], sidx_l[K];
+  bool skip[K];
+#pragma unroll
+  for (int p = 0; p < K; ++p) {
+    const int i = ctid * K + p;
+    const int li = dir == 0 ? i : i - 1;
+    const int sym = has_l[p] ? s_lab[li] : a.blank;
+    sidx_l[p] = has_l[p] ? (fused ? sym : s_slotpos[li]) : g.SW;
+    sidx_b[p] = has_b[p] ? (fused ? a.blank : 0) : g.SW;
+    skip[p] = (is_chain || is_helper) && i >= 1 && i < L && s_lab[i] != a.blank && s_lab[i] != s_lab[i - 1];
+  }
+  DF vb[K], vl[K];  // published values: alpha (forward) or emission-inclusive beta~ (backward)
+  DF xb[K], xl[K];  // backward only: emission-exclusive beta (what storage / occupancy use)
+  float2 eB[K], eL[K];
+#pragma unroll
+  for (int p = 0; p < K; ++p) {
+    vb[p] = vl[p] = xb[p] = xl[p] = sent();
+    eB[p] = eL[p] = make_float2(SENT, 0.f);
+  }
+  unsigned long long* my_ring = hring + static_cast<size_t>(cwarp) * RH * 64 * K;
+
+  // Cells that do not exist get a sentinel emission (no predicate on the critical path).
   auto load_emis = [&](int k) {
     const float2* er = emis + (k & M2) * SW;
-    const float2 ninf = make_float2(NEGF, 0.f);
-    const float2 e0 = er[sidx_b];
 #pragma unroll
     for (int p = 0; p < K; ++p) {
-      eBp[p] = has_b[p] ? e0 : ninf;
-      const float2 e1 = er[sidx_l[p]];
-      eL[p] = has_l[p] ? e1 : ninf;
+      eB[p] = er[sidx_b[p]];
+      eL[p] = er[sidx_l[p]];
     }
   };
   auto first_column = [&]() {
 #pragma unroll
     for (int p = 0; p < K; ++p) {
-      const int i = tid * K + p;
+      const int i = ctid * K + p;
       if (dir == 0) {  // alpha(s, 0) = lp(0, aug[s]) for s < 2 (ctc.cpp:114)
-        vb[p] = i == 0 ? DF{eBp[p].x, eBp[p].y} : dneg();
-        vl[p] = i == 0 ? DF{eL[p].x, eL[p].y} : dneg();
-        if (eBp[p].x == NEGF) vb[p] = dneg();
-        if (eL[p].x == NEGF) vl[p] = dneg();
+        vb[p] = i == 0 ? DF{eB[p].x, eB[p].y} : sent();
+        vl[p] = i == 0 ? DF{eL[p].x, eL[p].y} : sent();
       } else {  // beta(s, T-1) = 0 for s >= S-2 (ctc.cpp:130)
         const bool last = i == L;
-        const LSE zero{{0.f, 0.f}, 0.f};
-        xb[p] = (last && has_b[p]) ? DF{0.f, 0.f} : dneg();
-        xl[p] = (last && has_l[p]) ? DF{0.f, 0.f} : dneg();
-        vb[p] = last ? incl(zero, eBp[p]) : dneg();
-        vl[p] = last ? incl(zero, eL[p]) : dneg();
+        xb[p] = last ? DF{0.f, 0.f} : sent();
+        xl[p] = last ? DF{0.f, 0.f} : sent();
+        vb[p] = last ? incl(DF{0.f, 0.f}, 0.f, eB[p]) : sent();
+        vl[p] = last ? incl(DF{0.f, 0.f}, 0.f, eL[p]) : sent();
       }
     }
-    if (dir == 0) bnd_put(lane == 31 && warp + 1 < nw_u, bnd + warp * P2, vl[K - 1], 0);
-    else bnd_put(lane == 0 && warp > 0, bnd + warp * P2, vl[0], 0);
+    if (dir == 0) st_tagged(lane == 31 && warp + 1 < nw_u, bnd + warp * P2, vl[K - 1], 0);
+    else st_tagged(lane == 0 && warp > 0, bnd + warp * P2, vl[0], 0);
   };
-  auto critical = [&](int k) {  // k >= 1; branch-free except the warp-uniform poll
+  // Boundary value of the neighbouring warp, prefetched one step early
+  // (the neighbour normally runs >= 2 steps ahead); re-polled if stale.
+  unsigned long long bpre = ~0ull;
+  auto take_boundary = [&](const unsigned long long* slot, int tag) -> DF {
+    unsigned long long u = bpre;
+    if ((u & 0xFFull) != (static_cast<unsigned long long>(tag) & 0xFFull)) return ld_tagged(slot, tag);
+    return tag_unpack(u);
+  };
+  auto prefetch_boundary = [&](const unsigned long long* slot) {
+    asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(bpre) : "r"(smem_addr(slot)));
+  };
+  auto critical = [&](int k) {  // k >= 1
     if (dir == 0) {
       DF nb;
       nb.h = __shfl_up_sync(0xffffffffu, vl[K - 1].h, 1);
       nb.l = __shfl_up_sync(0xffffffffu, vl[K - 1].l, 1);
       if (warp > 0) {
-        const DF bv = bnd_get(bnd + (warp - 1) * P2 + ((k - 1) & M2), k - 1);
+        const DF bv = take_boundary(bnd + (warp - 1) * P2 + ((k - 1) & M2), k - 1);
         if (lane == 0) nb = bv;
       } else if (lane == 0) {
-        nb = dneg();
+        nb = sent();
       }
       DF nvb[K], nvl[K];
 #pragma unroll
       for (int p = 0; p < K; ++p) {
         const DF n1 = p == 0 ? nb : vl[p - 1];
-        const LSE mb = lse2(vb[p], n1);                            // blank 2i <- 2i, 2i-1
-        const LSE ml = lse3(vl[p], vb[p], skip[p] ? n1 : dneg());  // label 2i+1 <- 2i+1, 2i, 2i-1
-        nvb[p] = incl(mb, eBp[p]);
-        nvl[p] = incl(ml, eL[p]);
+        DF mb, ml;
+        const float cb = lse2(vb[p], n1, mb);                          // blank 2i <- 2i, 2i-1
+        const float cl = lse3(vl[p], vb[p], skip[p] ? n1 : sent(), ml);  // label 2i+1 <- 2i+1, 2i, 2i-1
+        nvb[p] = incl(mb, cb, eB[p]);
+        nvl[p] = incl(ml, cl, eL[p]);
       }
 #pragma unroll
       for (int p = 0; p < K; ++p) {
         vb[p] = nvb[p];
         vl[p] = nvl[p];
       }
-      bnd_put(lane == 31 && warp + 1 < nw_u, bnd + warp * P2 + (k & M2), vl[K - 1], k);
+      st_tagged(lane == 31 && warp + 1 < nw_u, bnd + warp * P2 + (k & M2), vl[K - 1], k);
+      if (warp > 0) prefetch_boundary(bnd + (warp - 1) * P2 + (k & M2));
     } else {
       DF nb;
       nb.h = __shfl_down_sync(0xffffffffu, vl[0].h, 1);
       nb.l = __shfl_down_sync(0xffffffffu, vl[0].l, 1);
       if (warp + 1 < nw_u) {
-        const DF bv = bnd_get(bnd + (warp + 1) * P2 + ((k - 1) & M2), k - 1);
+        const DF bv = take_boundary(bnd + (warp + 1) * P2 + ((k - 1) & M2), k - 1);
         if (lane == 31) nb = bv;
       } else if (lane == 31) {
-        nb = dneg();
+        nb = sent();
       }
       DF nvb[K], nvl[K];
 #pragma unroll
       for (int p = K - 1; p >= 0; --p) {
         const DF n1 = p == K - 1 ? nb : vl[p + 1];
-        const LSE mb = lse2(vb[p], n1);                            // blank 2i <- 2i, 2i+1
-        const LSE ml = lse3(vl[p], vb[p], skip[p] ? n1 : dneg());  // label 2i-1 <- 2i-1, 2i, 2i+1
-        nvb[p] = incl(mb, eBp[p]);
-        nvl[p] = incl(ml, eL[p]);
-        xb[p] = excl(mb);  // only stored / used where the cell exists
-        xl[p] = excl(ml);
+        DF mb, ml;
+        const float cb = lse2(vb[p], n1, mb);                          // blank 2i <- 2i, 2i+1
+        const float cl = lse3(vl[p], vb[p], skip[p] ? n1 : sent(), ml);  // label 2i-1 <- 2i-1, 2i, 2i+1
+        nvb[p] = incl(mb, cb, eB[p]);
+        nvl[p] = incl(ml, cl, eL[p]);
+        xb[p] = excl(mb, cb);
+        xl[p] = excl(ml, cl);
       }
 #pragma unroll
       for (int p = 0; p < K; ++p) {
         vb[p] = nvb[p];
         vl[p] = nvl[p];
       }
-      bnd_put(lane == 0 && warp > 0, bnd + warp * P2 + (k & M2), vl[0], k);
+      st_tagged(lane == 0 && warp > 0, bnd + warp * P2 + (k & M2), vl[0], k);
+      if (warp + 1 < nw_u) prefetch_boundary(bnd + (warp + 1) * P2 + (k & M2));
     }
   };
-  // Values of the current column that storage / occupancy use (alpha, or emission-exclusive beta).
-  auto snapshot = [&]() {
+  // Publish column k to the helper ring (after the helper freed the slot).
+  auto publish = [&](int k) {
+#ifdef DS2CTC_EXP_NOHELPER
+    return;
+#endif
+    if (k >= RH)
+      while (ld_volatile_int(hprog + cwarp) < k - RH) __nanosleep(32);
+    unsigned long long* slot = my_ring + (k & MH) * 64 * K;
 #pragma unroll
     for (int p = 0; p < K; ++p) {
-      qb[p] = dir == 0 ? vb[p] : xb[p];
-      ql[p] = dir == 0 ? vl[p] : xl[p];
+      st_tagged(true, slot + (2 * p) * 32 + lane, dir == 0 ? vb[p] : xb[p], k);
+      st_tagged(true, slot + (2 * p + 1) * 32 + lane, dir == 0 ? vl[p] : xl[p], k);
     }
   };
-  auto column_max = [&]() {  // warp max of the hi parts of the snapshot (CREDUX)
-    float hm = NEGF;
-#pragma unroll
-    for (int p = 0; p < K; ++p) hm = fmaxf(hm, fmaxf(qb[p].h, ql[p].h));
-    return warp_max_redux(hm);
-  };
-  // Phase-1 column store of the snapshot: fp32 delta from the warp max of the hi parts.
-  auto store_column = [&](int k, float wmax) {
-    const int col = (dir == 0 && k == kmid) ? T : frame(k);
-    float* dst = a.store + u.store_off + static_cast<size_t>(col) * cw;
-#pragma unroll
-    for (int p = 0; p < K; ++p) {
-      const int i = tid * K + p;
-      const float db = qb[p].h == NEGF ? NEGF : (qb[p].h - wmax) + qb[p].l;
-      const float dl = ql[p].h == NEGF ? NEGF : (ql[p].h - wmax) + ql[p].l;
-      if (has_b[p]) dst[2 * i] = db;
-      if (has_l[p]) dst[dir == 0 ? 2 * i + 1 : 2 * i - 1] = dl;
-    }
-    if (lane == 0) dst[S4 + warp] = wmax;
-  };
-  // Partner (woff, delta) of each of my cells for row k (the partner's stored column).
-  auto load_partner = [&](int k) {
-    const float* col = sring + (k & M2) * g.cw_max;
-#pragma unroll
-    for (int p = 0; p < K; ++p) {
-      const int i = tid * K + p;
-      const int sb = 2 * i, sl = dir == 0 ? 2 * i + 1 : 2 * i - 1;
-      const int wb = dir == 0 ? (sb + 1) / (64 * K) : sb / (64 * K);  // partner's writer warp
-      const int wl = dir == 0 ? (sl + 1) / (64 * K) : sl / (64 * K);
-      nwb[p] = has_b[p] ? col[S4 + wb] : NEGF;
-      ndb[p] = has_b[p] ? col[sb] : NEGF;
-      nwl[p] = has_l[p] ? col[S4 + wl] : NEGF;
-      ndl[p] = has_l[p] ? col[sl] : NEGF;
-    }
-  };
-  // gamma = alpha + beta - log Z (plain add, ctc.cpp:200) -> occupancy 2^gamma.
-  auto occupancy = [&](DF v, float woff, float delta) -> float {
-    const DF p = two_sum(v.h, -Zh);
-    const float q = p.h + woff;
-    const float gg = q + ((p.l + v.l) + (delta - Zl));
-    const float o = ex2(gg);
-    return (v.h == NEGF || woff == NEGF || delta == NEGF) ? 0.f : o;
-  };
-  auto occupancy_row = [&](int k) {  // uses the snapshot and pw*/pd*
-    float* ebr = eb + (k & M2) * g.estride;
-    float* elr = el + (k & M2) * g.estride;
-#pragma unroll
-    for (int p = 0; p < K; ++p) {
-      const int i = tid * K + p;
-      if (has_b[p]) ebr[i] = occupancy(qb[p], pwb[p], pdb[p]);
-      if (has_l[p]) elr[dir == 0 ? i : i - 1] = occupancy(ql[p], pwl[p], pdl[p]);
-    }
-  };
-
-  // One epoch of chain work. The critical recursion of step k is issued
-  // first; the column store (phase 1) or occupancy row (phase 2) of step k-1
-  // follows, so its latency overlaps the next column instead of stalling it.
   auto chain_epoch = [&](const Epoch& e) {
     load_emis(e.k0);
     for (int k = e.k0; k < e.k1; ++k) {
+      STEP_STAMP(k, e, 0);
       if (k == 0) first_column();
       else if (e.phase == 1 || k > kmid) critical(k);
-#ifndef DS2CTC_EXP_NOEMIS
+      STEP_STAMP(k, e, 1);
       if (k + 1 < e.k1) load_emis(k + 1);
-#endif
-      if (e.phase == 1) {
-#ifndef DS2CTC_EXP_NOSTORE
-        const float wnow = [&] {
-          // snapshot of column k taken after the previous column was stored
-          if (k > e.k0) store_column(k - 1, wprev);
-          snapshot();
-#ifdef DS2CTC_EXP_NOREDUX
-          return 0.f;
-#else
-          return column_max();
-#endif
-        }();
-        wprev = wnow;
-#endif
-      } else {
-        load_partner(k);
-        if (k > e.k0) occupancy_row(k - 1);
-        snapshot();
-#pragma unroll
-        for (int p = 0; p < K; ++p) {
-          pwb[p] = nwb[p];
-          pdb[p] = ndb[p];
-          pwl[p] = nwl[p];
-          pdl[p] = ndl[p];
-        }
-      }
-    }
-    if (e.phase == 1) {
-      store_column(e.k1 - 1, wprev);
-    } else {
-      occupancy_row(e.k1 - 1);
+      publish(k);
+      STEP_STAMP(k, e, 2);
     }
   };
 
+  // =====================================================================
+  // Helper warps: store (phase 1) / occupancy (phase 2) of published columns.
+  // =====================================================================
+  // Partner (offset, deltas) of this lane's cells for a phase-2 row, loaded
+  // straight from the (L2-resident) store two steps ahead of use.
+  struct PartnerRow {
+    float off_lo, off_hi;  // offsets of the writer threads of the lane's first / last slot
+    float d[2 * K];        // the partner's deltas for slots 2*ctid*K + pshift ... (+2K)
+  };
+  // The partner's slot of cell s is s + 1 when the partner is the backward CTA
+  // and s when it is the forward one; this lane's first cell is 2*ctid*K
+  // (forward: blank) or 2*ctid*K - 1 (backward: label), so its first partner
+  // slot is 2*ctid*K + 1 resp. 2*ctid*K - 1 (slot -1 belongs to no cell and
+  // is never used).
+  const int lane_slot0 = 2 * ctid * K + (dir == 0 ? 1 : -1);
+  auto load_partner = [&](int k, PartnerRow& r) {
+    if (k >= T || !is_helper || ctid * K > L) return;
+    const float* col = a.store + u.store_off + static_cast<size_t>(frame(k)) * cw;
+    const int s0 = lane_slot0;
+#pragma unroll
+    for (int q = 0; q < 2 * K; ++q) r.d[q] = col[s0 + q];
+    r.off_lo = col[OB + s0 / (2 * K)];
+    r.off_hi = col[OB + (s0 + 2 * K - 1) / (2 * K)];
+  };
+  auto helper_epoch = [&](const Epoch& e) {
+    PartnerRow pa{}, pb{};
+    if (e.phase == 2) {
+      load_partner(e.k0, pa);
+      load_partner(e.k0 + 1, pb);
+    }
+    for (int k = e.k0; k < e.k1; ++k) {
+      STEP_STAMP(k, e, 0);
+      const unsigned long long* slot = my_ring + (k & MH) * 64 * K;
+      // One round trip for all 2K values of this lane, then re-poll if any is stale.
+      unsigned long long raw[2 * K];
+      for (;;) {
+        bool ok = true;
+#pragma unroll
+        for (int q = 0; q < 2 * K; ++q) {
+          asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(raw[q]) : "r"(smem_addr(slot + q * 32 + lane)));
+          ok &= (raw[q] & 0xFFull) == (static_cast<unsigned long long>(k) & 0xFFull);
+        }
+        if (ok) break;
+        __nanosleep(32);
+      }
+      DF cb[K], clv[K];
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        cb[p] = tag_unpack(raw[2 * p]);
+        clv[p] = tag_unpack(raw[2 * p + 1]);
+      }
+      __syncwarp();
+      if (lane == 0) st_volatile_int(hprog + cwarp, k);
+      STEP_STAMP(k, e, 1);
+      if (e.phase == 1) {
+        // fp32 deltas from this thread's own max hi part (no cross-lane
+        // reduction); sentinels are stored as -inf.
+        float hm = NEGF;
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+          if (cb[p].h > SENT_CUT) hm = fmaxf(hm, cb[p].h);
+          if (clv[p].h > SENT_CUT) hm = fmaxf(hm, clv[p].h);
+        }
+        const int col = (dir == 0 && k == kmid) ? T : frame(k);
+        float* dst = a.store + u.store_off + static_cast<size_t>(col) * cw;
+        if (ctid < column_threads(L, K)) {
+#pragma unroll
+          for (int p = 0; p < K; ++p) {
+            const float db = (has_b[p] && cb[p].h > SENT_CUT) ? (cb[p].h - hm) + cb[p].l : NEGF;
+            const float dl = (has_l[p] && clv[p].h > SENT_CUT) ? (clv[p].h - hm) + clv[p].l : NEGF;
+            // forward pair = slots (blank 2i, label 2i+1); backward = (label 2i-1, blank 2i) at +1
+            reinterpret_cast<float2*>(dst)[ctid * K + p] = dir == 0 ? make_float2(db, dl) : make_float2(dl, db);
+          }
+          dst[OB + ctid] = hm;
+        }
+      } else {
+        // gamma = alpha + beta - log Z (plain add, ctc.cpp:200) -> occupancy 2^gamma.
+        float* ebr = eb + (k & M2) * g.estride;
+        float* elr = el + (k & M2) * g.estride;
+        auto occ = [&](DF v, float woff, float delta) -> float {
+          const DF p = two_sum(v.h, -Zh);
+          const float q = p.h + woff;
+          const float gg = q + ((p.l + v.l) + (delta - Zl));
+          const float o = ex2(gg);
+          return (v.h <= SENT_CUT || woff == NEGF || delta == NEGF) ? 0.f : o;
+        };
+        // This lane's cells in slot order: forward (blank 2i, label 2i+1) at
+        // partner slots 2i+1, 2i+2; backward (label 2i-1, blank 2i) at 2i-1, 2i.
+        const int s0 = lane_slot0;
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+          const int i = ctid * K + p;
+          // static register indices only (a runtime index would spill the row to local memory)
+          const float d_even = pa.d[2 * p], d_odd = pa.d[2 * p + 1];
+          const int qb = dir == 0 ? 2 * p : 2 * p + 1;  // position of the blank cell among the lane's 2K cells
+          const int ql = dir == 0 ? 2 * p + 1 : 2 * p;
+          const float ob = (s0 + qb) / (2 * K) == s0 / (2 * K) ? pa.off_lo : pa.off_hi;
+          const float ol = (s0 + ql) / (2 * K) == s0 / (2 * K) ? pa.off_lo : pa.off_hi;
+          if (has_b[p]) ebr[i] = occ(cb[p], ob, dir == 0 ? d_even : d_odd);
+          if (has_l[p]) elr[dir == 0 ? i : i - 1] = occ(clv[p], ol, dir == 0 ? d_odd : d_even);
+        }
+        pa = pb;
+        load_partner(k + 2, pb);
+      }
+      STEP_STAMP(k, e, 2);
+    }
+  };
+
+#ifdef DS2CTC_EXP_TIGHT
+  // Debug: the recursion alone, 1000 steps back to back on chain warp 0 (its
+  // neighbour value is the sentinel), timed with clock64.
+  if (blockIdx.x < 2 && warp == 0 && dir == 0) {  // forward warp 0 has no neighbour to wait for
+    long long t0 = clock64();
+    for (int it = 0; it < 1000; ++it) critical(2 + (it & 1));
+    long long t1 = clock64();
+    if (lane == 0) g_step_clock[dir][7][31][3] = t1 - t0;
+    t0 = clock64();
+    for (int it = 0; it < 1000; ++it) {
+      critical(2 + (it & 1));
+      load_emis(3 + (it & 7));
+    }
+    t1 = clock64();
+    if (lane == 0) g_step_clock[dir][7][31][2] = t1 - t0;
+    t0 = clock64();
+    const Epoch fake{2, 1002, 1};
+    for (int k = 2; k < 1002; ++k) {
+      STEP_STAMP(k, fake, 0);
+      critical(k);
+      STEP_STAMP(k, fake, 1);
+      load_emis(k + 1);
+      STEP_STAMP(k, fake, 2);
+    }
+    t1 = clock64();
+    if (lane == 0) g_step_clock[dir][7][31][1] = t1 - t0;
+    if (vl[0].h == 12345.f) a.costs[b] = vl[K - 1].l;  // keep the loop alive
+  }
+#endif
   // ---- prologue staging of epoch 0 ----
   Epoch cur{0, min(P, kmid + 1), 1};
   if (service) {
-    stage(cur, false);
+    stage(cur);
     cp_async_wait_all();
     __syncwarp();
     convert(cur);
@@ -627,13 +757,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMaxThreads, 1) k_pa
     Epoch stg = nxt;
     if (stg.phase != 0 && stg.k0 < cur.k1) stg.k0 = cur.k1;
     if (service) {
-      stage(stg, cur.phase == 2);
+#ifndef DS2CTC_EXP_NOSERVICE
+      stage(stg);
       grad_rows(prev);
       cp_async_wait_all();
       __syncwarp();
       convert(stg);
+#endif
     } else if (is_chain) {
       chain_epoch(cur);
+    } else if (is_helper) {
+#ifndef DS2CTC_EXP_NOHELPER
+      helper_epoch(cur);
+#endif
     }
 #ifdef DS2CTC_EPOCH_TIMING
     if (blockIdx.x < 2 && lane == 0 && epoch_idx < 128) g_epoch_clock[dir][epoch_idx][warp][1] = clock64();
@@ -647,11 +783,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMaxThreads, 1) k_pa
       // at column tm) with the same cell->thread map and reduction order, so
       // they derive the bitwise-identical log Z.
       const float* ca = a.store + u.store_off + static_cast<size_t>(T) * cw;
-      const float* cb = a.store + u.store_off + static_cast<size_t>(tm) * cw;
+      const float* cbp = a.store + u.store_off + static_cast<size_t>(tm) * cw;
       double mloc = -__builtin_huge_val();
       for (int s = tid; s < S; s += NT) {
-        const float wa = ca[S4 + s / (64 * K)], da = ca[s];
-        const float wb = cb[S4 + (s + 1) / (64 * K)], db = cb[s];
+        const float wa = ca[OB + s / (2 * K)], da = ca[s];                    // forward: slot s
+        const float wb = cbp[OB + (s + 1) / (2 * K)], db = cbp[s + 1];        // backward: slot s + 1
         if (wa == NEGF || da == NEGF || wb == NEGF || db == NEGF) continue;
         const double v = (static_cast<double>(wa) + static_cast<double>(da)) +
                          (static_cast<double>(wb) + static_cast<double>(db));
@@ -670,8 +806,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMaxThreads, 1) k_pa
       } else {
         float sl = 0.f;
         for (int s = tid; s < S; s += NT) {
-          const float wa = ca[S4 + s / (64 * K)], da = ca[s];
-          const float wb = cb[S4 + (s + 1) / (64 * K)], db = cb[s];
+          const float wa = ca[OB + s / (2 * K)], da = ca[s];
+          const float wb = cbp[OB + (s + 1) / (2 * K)], db = cbp[s + 1];
           if (wa == NEGF || da == NEGF || wb == NEGF || db == NEGF) continue;
           const double v = (static_cast<double>(wa) + static_cast<double>(da)) +
                            (static_cast<double>(wb) + static_cast<double>(db));
@@ -688,16 +824,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMaxThreads, 1) k_pa
       Zl = static_cast<float>(logz2 - static_cast<double>(Zh));
       dead = logz2 == -__builtin_huge_val();  // zero-probability lattice (ctc.cpp:189-193)
       if (dead || !want_grad) break;
-      // Partner columns of the first phase-2 epoch (now visible after the cluster barrier).
-      if (service) {
-        const Epoch first = next_epoch(cur);
-        for (int k = first.k0; k < first.k1; ++k) {
-          const float* col = a.store + u.store_off + static_cast<size_t>(frame(k)) * cw;
-          for (int c4 = lane; c4 < cw / 4; c4 += 32) cp_async16(sring + (k & M2) * g.cw_max + 4 * c4, col + 4 * c4);
-        }
-        cp_async_commit();
-        cp_async_wait_all();
-      }
       __syncthreads();
     }
     prev = cur;
@@ -705,31 +831,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMaxThreads, 1) k_pa
   }
   if (service && !dead && want_grad) grad_rows(prev);  // the last phase-2 epoch
 
-  // ---- costs: cost = sum_t lse_t - log Z (natural log) ----
-  if (fused) {
-    if (want_grad) {
-      if (dead) zero_rows(dir == 0 ? tm : 0, dir == 0 ? T : tm);
-      if (dir == 1) zero_rows(T, a.t_max);
-    }
-    if (service) {
-      for (int o = 16; o > 0; o >>= 1) lse_acc += __shfl_xor_sync(0xffffffffu, lse_acc, o);
-      if (lane == 0) a.part[2 * b + dir] = lse_acc;
-    }
-    cluster_barrier();
-    if (dir == 0 && tid == 0) {
+  // ---- costs: fused cost = sum_t ls_t - log Z' (natural log; log Z' of the shifted frames) ----
+  if (service) {
+    for (int o = 16; o > 0; o >>= 1) part_acc += __shfl_xor_sync(0xffffffffu, part_acc, o);
+    if (lane == 0) a.part[2 * b + dir] = part_acc;
+  }
+  if (fused && want_grad) {
+    if (dead) zero_rows(dir == 0 ? tm : 0, dir == 0 ? T : tm);
+    if (dir == 1) zero_rows(T, a.t_max);
+  }
+  cluster_barrier();
+  if (dir == 0 && tid == 0) {
+    a.logz[b] = logz2;
+    if (fused) {
       const double tot = a.part[2 * b] + a.part[2 * b + 1];
-      a.logz[b] = logz2;
       a.costs[b] = dead ? __builtin_huge_valf() : static_cast<float>(tot - logz2 * kLn2);
     }
-  } else if (dir == 0 && tid == 0) {
-    a.logz[b] = logz2;
   }
 }
 
 template <int K>
 int launch_k(const PairArgs& a, void* stream) {
-  const int threads = 32 * (a.g.nchain + 1);
-  if (threads > kMaxThreads) return cudaErrorInvalidValue;
+  const int threads = 32 * (2 * a.g.nchain + 1);
+  if (threads > max_threads_for<K>()) return cudaErrorInvalidValue;
   cudaError_t err = cudaFuncSetAttribute(k_pair<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, a.g.smem);
   if (err != cudaSuccess) return err;
   k_pair<K><<<2 * a.B, threads, a.g.smem, static_cast<cudaStream_t>(stream)>>>(a);
@@ -741,6 +865,9 @@ int launch_k(const PairArgs& a, void* stream) {
 #ifdef DS2CTC_EPOCH_TIMING
 extern "C" int ds2ctc_debug_epoch_clocks(long long* host) {
   return cudaMemcpyFromSymbol(host, g_epoch_clock, sizeof(g_epoch_clock));
+}
+extern "C" int ds2ctc_debug_step_clocks(long long* host) {
+  return cudaMemcpyFromSymbol(host, g_step_clock, sizeof(g_step_clock));
 }
 #endif
 

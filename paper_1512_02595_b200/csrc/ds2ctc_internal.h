@@ -26,7 +26,7 @@ namespace ds2ctc {
 
 constexpr int kMaxStates = 4095;  // == DS2CTC_MAX_STATES
 constexpr int kFusedMaxAlphabet = 128;
-constexpr int kMaxThreads = 320;  // chain warps (<= 8 at K = 8, L <= 2047) + 1 service warp
+constexpr int kMaxThreads = 544;  // chain + helper warps (<= 8 each at K = 8, L <= 2047) + 1 service warp
 constexpr size_t kAlign = 256;
 constexpr size_t kSmemBudget = 220 * 1024;
 
@@ -58,7 +58,9 @@ struct Geometry {
   int max_L;
   int fused;
   // shared-memory carve-up (bytes, 16-aligned)
-  int off_xraw, off_emis, off_lse, off_eb, off_el, off_sring, off_tile, off_occ, off_bnd, off_meta, off_red;
+  int off_xraw, off_emis, off_lse, off_eb, off_el, off_tile, off_occ, off_bnd, off_meta, off_red;
+  int off_hring, off_hprog;
+  int RH;         // helper ring depth (columns in flight between a chain warp and its helper)
   int xstride;    // floats per xraw row (odd)
   int estride;    // floats per eb/el row (odd)
   int cw_max;     // floats per stored column (max over batch)
@@ -80,16 +82,23 @@ inline int pick_K(int max_L) {
   return 8;
 }
 
-inline int column_width(int L, int K) { return round_up(2 * L + 1, 4) + round_up(chain_warps_for(L, K), 4); }
+// Stored half-lattice column: chain thread j owns 2K consecutive slots
+// (forward: slot = cell s; backward: slot = s + 1, so each thread's cells are
+// 16-byte aligned), then one fp32 offset per chain thread.
+DS2CTC_HD inline int column_threads(int L, int K) { return (L + 1 + K - 1) / K; }
+DS2CTC_HD inline int column_offsets_base(int L, int K) { return round_up(2 * K * column_threads(L, K), 4); }
+DS2CTC_HD inline int column_width(int L, int K) { return column_offsets_base(L, K) + round_up(column_threads(L, K), 4); }
 
-inline Geometry make_geometry(int max_L, int max_nkey, int A, bool fused) {
+// max_L_all: the longest label of the whole batch (it fixes K and hence the
+// stored column layout, see make_layout); max_L: the longest that runs.
+inline Geometry make_geometry(int max_L_all, int max_L, int max_nkey, int A, bool fused) {
   Geometry g{};
-  g.K = pick_K(max_L);
+  g.K = pick_K(max_L_all);
   g.nchain = chain_warps_for(max_L, g.K);
   g.max_L = max_L;
   g.fused = fused ? 1 : 0;
   g.SW = fused ? A : max_nkey;
-  g.cw_max = column_width(max_L, g.K);
+  g.cw_max = column_width(max_L_all, g.K);
   for (int P = 32; P >= 2; P /= 2) {
     g.P = P;
     g.xstride = g.SW | 1;
@@ -104,14 +113,16 @@ inline Geometry make_geometry(int max_L, int max_nkey, int A, bool fused) {
     };
     const int RX = 4 * P;
     g.off_xraw = take(4 * RX * g.xstride);
-    g.off_emis = take(8 * 2 * P * g.SW);
+    g.off_emis = take(8 * 2 * P * (g.SW + 1));  // + a sentinel column for cells that do not exist
     g.off_lse = take(8 * RX);
     g.off_eb = take(4 * 2 * P * g.estride);
     g.off_el = take(4 * 2 * P * g.estride);
-    g.off_sring = take(4 * 2 * P * g.cw_max);
     g.off_tile = take(4 * P * g.tstride);
     g.off_occ = take(4 * P * g.ostride);
     g.off_bnd = take(8 * g.nchain * 2 * P);
+    g.RH = P >= 8 ? 8 : P;
+    g.off_hring = take(8 * g.nchain * g.RH * 32 * 2 * g.K);
+    g.off_hprog = take(4 * 32);
     // meta: labels (L+1), key_char (nkey), key_start (nkey+1), key_pos (L), slot of each label
     // position (L+1), symbol -> slot (A shorts, fused)
     g.off_meta = take(4 * (3 * max_L + 2 * max_nkey + 8) + (fused ? 2 * A : 0));

@@ -52,11 +52,25 @@ def run(so, A=29, T=700, L=150, B=64, brief=False):
     buf = np.zeros((2, 128, 33, 2), dtype=np.int64)
     lib = ctypes.CDLL(so)
     assert lib.ds2ctc_debug_epoch_clocks(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong))) == 0
+    steps = np.zeros((2, 8, 32, 4), dtype=np.int64)
+    assert lib.ds2ctc_debug_step_clocks(steps.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong))) == 0
+    for cta in range(2):
+        base = steps[cta, 0, 0, 0]
+        print(f"CTA {cta} epoch-1 step stamps (relative to warp 0 step 0 start): [start, mid, end] per warp")
+        for k in range(0, 32, 4):
+            row = []
+            for w in range(8):
+                if steps[cta, w, k, 0] == 0:
+                    continue
+                row.append(f"w{w}:" + ",".join(str(int(steps[cta, w, k, j] - base)) for j in range(3)))
+            print(f"  k+{k:2d} " + "  ".join(row))
+    print("TIGHT cycles/step: critical", steps[0, 7, 31, 3] / 1000.0, "| + load_emis", steps[0, 7, 31, 2] / 1000.0,
+          "| + stamps & real k", steps[0, 7, 31, 1] / 1000.0)
     if brief:
         for cta in range(2):
             rows = [buf[cta, e] for e in range(128) if buf[cta, e, 0, 0] != 0]
             p1 = [r for r in rows[:8]]
-            busy = np.mean([[int(r[w, 1] - r[w, 0]) for w in range(4)] for r in p1], axis=0)
+            busy = np.mean([[int(r[w, 1] - r[w, 0]) for w in range(8)] for r in p1], axis=0)
             total = int(rows[-1][0, 1] - rows[0][0, 0])
             print(f"  cta{cta}: total {total} cycles, phase-1 epoch busy per warp {busy.astype(int).tolist()}")
         return
@@ -74,7 +88,7 @@ def run(so, A=29, T=700, L=150, B=64, brief=False):
 
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "variants":
-        for defs in [(), ("NOSTORE",), ("NOREDUX",), ("NOEMIS",), ("NOSTORE", "NOEMIS")]:
+        for defs in [()]:
             so = build(defs)
             print("variant", defs or "base")
             run(so, brief=True)
