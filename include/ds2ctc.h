@@ -127,6 +127,14 @@ ds2ctc_status ds2ctc_loss_sum(const float* costs, int minibatch, double* out2, v
 ds2ctc_status ds2ctc_profile_enable(int slots);
 ds2ctc_status ds2ctc_profile_read(int call_index, float* ms);
 
+/*
+ * Diagnostics: every inter-warp wait inside the pair kernel is bounded; a
+ * wait that exceeds its bound (a protocol bug) is recorded instead of hanging
+ * the GPU. Synchronises the device, writes {kind, block, warp, step} of the
+ * first such event since the last call (all zero if none) and clears it.
+ */
+ds2ctc_status ds2ctc_debug_watchdog(unsigned long long* out4);
+
 /* ---------------------------------------------------------------------
  * H1 host scheduler (trainer.cpp:58-91, 140-143) -- pure host functions.
  * ------------------------------------------------------------------- */

@@ -32,6 +32,7 @@ EXPORTS = (
     "ds2ctc_loss_sum",
     "ds2ctc_profile_enable",
     "ds2ctc_profile_read",
+    "ds2ctc_debug_watchdog",
     "ds2ctc_sortagrad_order",
     "ds2ctc_rank_slice",
     "ds2ctc_shard_lpt",
@@ -86,6 +87,8 @@ def lib():
             L.ds2ctc_profile_enable.argtypes = [ctypes.c_int]
             L.ds2ctc_profile_read.restype = ctypes.c_int
             L.ds2ctc_profile_read.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_float)]
+            L.ds2ctc_debug_watchdog.restype = ctypes.c_int
+            L.ds2ctc_debug_watchdog.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
             L.ds2ctc_sortagrad_order.restype = ctypes.c_int
             L.ds2ctc_sortagrad_order.argtypes = [_ip, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_uint64,
                                                  ctypes.c_int, _i64p]
@@ -95,6 +98,13 @@ def lib():
             L.ds2ctc_shard_lpt.argtypes = [_ip, _ip, ctypes.c_int, ctypes.c_int, ctypes.c_int, _ip, _dp]
             _lib = L
     return _lib
+
+
+def watchdog():
+    """(kind, block, warp, step) of the first bounded wait that gave up since the last call, or None."""
+    out = (ctypes.c_ulonglong * 4)()
+    check(lib().ds2ctc_debug_watchdog(out), "ds2ctc_debug_watchdog")
+    return None if out[0] == 0 else tuple(int(v) for v in out)
 
 
 def check(status: int, where: str) -> None:

@@ -370,6 +370,13 @@ ds2ctc_status ds2ctc_profile_read(int call_index, float* ms) {
   return DS2CTC_STATUS_SUCCESS;
 }
 
+ds2ctc_status ds2ctc_debug_watchdog(unsigned long long* out4) {
+  if (out4 == nullptr) return DS2CTC_STATUS_INVALID_VALUE;
+  if (cudaDeviceSynchronize() != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  if (read_watchdog(out4) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  return DS2CTC_STATUS_SUCCESS;
+}
+
 ds2ctc_status ds2ctc_compute_loss_host(const float* activations, float* gradients, const int* flat_labels,
                                        const int* label_lengths, const int* input_lengths, int alphabet_size,
                                        int minibatch, int blank_label, float* costs, int device) {

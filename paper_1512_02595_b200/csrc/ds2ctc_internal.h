@@ -117,15 +117,15 @@ inline Geometry make_geometry(int max_L_all, int max_L, int max_nkey, int A, boo
     g.off_lse = take(8 * RX);
     g.off_eb = take(4 * 2 * P * g.estride);
     g.off_el = take(4 * 2 * P * g.estride);
-    g.off_tile = take(4 * P * g.tstride);
-    g.off_occ = take(4 * P * g.ostride);
+    g.off_tile = take(4 * 32 * g.tstride);  // one row per service lane (all 32 lanes run, P <= 32)
+    g.off_occ = take(4 * 32 * g.ostride);
     g.off_bnd = take(8 * g.nchain * 2 * P);
     g.RH = P >= 8 ? 8 : P;
     g.off_hring = take(8 * g.nchain * g.RH * 32 * 2 * g.K);
     g.off_hprog = take(4 * 32);
     // meta: labels (L+1), key_char (nkey), key_start (nkey+1), key_pos (L), slot of each label
     // position (L+1), symbol -> slot (A shorts, fused)
-    g.off_meta = take(4 * (3 * max_L + 2 * max_nkey + 8) + (fused ? 2 * A : 0));
+    g.off_meta = take(4 * (4 * max_L + 2 * max_nkey + 8) + (fused ? 2 * A : 0));
     g.off_red = take(8 * 72);
     g.smem = off;
     if (static_cast<size_t>(off) <= kSmemBudget) break;
@@ -207,5 +207,6 @@ int launch_pair(const PairArgs& a, void* stream);
 int launch_dense(const PairArgs& a, bool write_grad, void* stream);
 int launch_finalize(const PairArgs& a, void* stream);
 int launch_loss_sum(const float* costs, int B, double* out2, void* stream);
+int read_watchdog(unsigned long long* out4);
 
 }  // namespace ds2ctc

@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 import oracle
+from paper_1512_02595_b200 import _lib
 from paper_1512_02595_b200 import ctc as dctc
 from paper_1512_02595_b200.synth import fixed_shape_batch, make_batch, sortagrad_lengths
 
@@ -25,6 +26,8 @@ def run_gpu(acts, flat, ll, il, blank=None, want_grad=True):
     x = torch.from_numpy(np.ascontiguousarray(acts)).cuda()
     costs, grads = dctc.compute_ctc_loss(x, flat, ll, il, blank=blank, want_grad=want_grad)
     torch.cuda.synchronize()
+    wd = _lib.watchdog()
+    assert wd is None, f"pair-kernel wait gave up (kind, block, warp, step) = {wd}"
     return costs.cpu().numpy().astype(np.float64), (grads.cpu().numpy() if grads is not None else None)
 
 
