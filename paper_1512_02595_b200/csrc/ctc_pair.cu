@@ -29,15 +29,15 @@
 // Warp roles. Chain thread i owns label pairs i*K .. i*K+K-1 (forward pair j
 // = (blank 2j, label 2j+1); backward pair j = (label 2j-1, blank 2j)), so a
 // pair needs ONE value from its neighbour per step: a warp shuffle, or,
-// across warps, a tagged shared-memory ring (no CTA barrier per step). Chain
-// warps do only the recursion and publish each column to a tagged ring; a
-// helper warp per chain warp (same lanes, same cells) turns published
-// columns into stored deltas (phase 1) or occupancies (phase 2) using the
-// SM sub-partition issue slots the latency-bound chain leaves idle. A
-// service warp stages logits (cp.async) and the partner's columns, computes
-// the per-frame statistics and emissions, and turns occupancy rows into
-// gradient rows (softmax - occupancy, ctc.cpp:69-79) one epoch behind. All
-// warps meet at a CTA barrier every P steps (an epoch).
+// across warps, a tagged shared-memory slot (no CTA barrier per step). In the
+// same basic block as step k a chain warp finishes column k - 1: stored
+// deltas (phase 1) or occupancies from the partner's stored half, which a
+// per-thread cp.async stream fetches a few steps ahead (phase 2); the
+// scheduler fills the recursion's latency gaps with that work. One service
+// warp (its own SM sub-partition) stages logits (cp.async), computes the
+// per-frame statistics and emissions, and turns occupancy rows into gradient
+// rows (softmax - occupancy, ctc.cpp:69-79) one epoch behind. All warps meet
+// at a CTA barrier every P steps (an epoch).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -54,6 +54,7 @@ constexpr double kLn2 = 0.69314718055994530942;
 constexpr float NEGF = -__builtin_huge_valf();
 constexpr float SENT = -1e30f;     // "-inf" inside the recursion
 constexpr float SENT_CUT = -1e29f;  // below this a value is -inf
+constexpr double kSentCutD = -1e29;
 
 struct DF {
   float h, l;
@@ -148,6 +149,27 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
 }
 
+__device__ __forceinline__ void cp_async16_if(bool pred, void* dst, const void* src) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p cp.async.cg.shared.global [%0], [%1], 16;\n\t}" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(static_cast<unsigned>(pred))
+      : "memory");
+}
+
+__device__ __forceinline__ void cp_async4_if(bool pred, void* dst, const void* src) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p cp.async.ca.shared.global [%0], [%1], 4;\n\t}" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(static_cast<unsigned>(pred))
+      : "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
@@ -204,16 +226,6 @@ __device__ __forceinline__ DF ld_tagged(const unsigned long long* slot, int tag,
   return tag_unpack(u);
 }
 
-__device__ __forceinline__ int ld_volatile_int(const int* p) {
-  int v;
-  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)));
-  return v;
-}
-
-__device__ __forceinline__ void st_volatile_int(int* p, int v) {
-  asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v));
-}
-
 #ifdef DS2CTC_EPOCH_TIMING
 // Debug build only (tools/epoch_timing): per-epoch clock64 of every warp of the
 // first cluster, [cta][epoch][warp][start, end].
@@ -222,7 +234,8 @@ __device__ long long g_epoch_clock[2][128][33][2];
 __device__ long long g_step_clock[2][8][32][4];
 #define STEP_STAMP(k, e, pt)                                                                            \
   do {                                                                                                  \
-    if (blockIdx.x < 2 && lane == 0 && warp < 8 && (e).k0 == P && (k) - (e).k0 < 32)                   \
+    if (blockIdx.x < 2 && lane == 0 && warp < 7 && (e).phase == 2 && (e).k0 == k2s + 2 * P &&           \
+        (k) - (e).k0 < 32)                                                                              \
       g_step_clock[dir][warp][(k) - (e).k0][pt] = clock64();                                            \
   } while (0)
 #else
@@ -236,18 +249,19 @@ struct Epoch {
   int k0, k1, phase;  // phase 0 = none
 };
 
-// K <= 4 keeps at most three chain warps (7 warps per CTA, full register file);
-// K = 6, 8 (labels longer than 384) may use up to eight.
+// K <= 4 keeps at most three chain warps (4 warps per CTA); K = 6, 8 (labels
+// longer than 384) may use up to eight.
 template <int K>
 constexpr int max_threads_for() {
-  return K <= 4 ? 32 * 7 : kMaxThreads;
+  return K <= 4 ? 32 * 4 : kMaxThreads;
 }
 
-template <int K>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(max_threads_for<K>(), 1) k_pair(PairArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
+// DIR 0: alpha forward (cluster rank 0), 1: beta backward (rank 1); a
+// compile-time direction keeps every per-cell register index static.
+template <int K, int DIR>
+__device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem) {
   const Geometry& g = a.g;
-  const int dir = static_cast<int>(cluster_rank());  // 0: alpha forward, 1: beta backward
+  constexpr int dir = DIR;
   const int b = a.order[blockIdx.x >> 1];
   const UttDesc u = a.desc[b];
   const int tid = threadIdx.x;
@@ -279,7 +293,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(max_threads_for<K>()
   const int T = u.T, L = u.L, S = u.S, tm = u.tm;
   const int P = g.P, RX = 4 * P, P2 = 2 * P;  // powers of two
   const int MX = RX - 1, M2 = P2 - 1;
-  const int RH = g.RH, MH = g.RH - 1;  // power of two
   const int OB = column_offsets_base(L, K);  // per-thread offsets of a stored column start here
   const int cw = u.col_w;
   const int nw_u = chain_warps_for(L, K);  // chain warps this utterance uses
@@ -297,8 +310,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(max_threads_for<K>()
   float* tile = reinterpret_cast<float*>(smem + g.off_tile);
   float* occs = reinterpret_cast<float*>(smem + g.off_occ);
   unsigned long long* bnd = reinterpret_cast<unsigned long long*>(smem + g.off_bnd);
-  unsigned long long* hring = reinterpret_cast<unsigned long long*>(smem + g.off_hring);
-  int* hprog = reinterpret_cast<int*>(smem + g.off_hprog);
   int* s_lab = reinterpret_cast<int*>(smem + g.off_meta);
   int* s_kchar = s_lab + (L + 1);
   int* s_kstart = s_kchar + u.nkey;
@@ -316,8 +327,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(max_threads_for<K>()
   if (fused)
     for (int c = tid; c < a.A; c += NT) s_slot[c] = -1;
   for (int q = tid; q < NCW * P2; q += NT) bnd[q] = ~0ull;
-  for (int q = tid; q < NCW * RH * 64 * K; q += NT) hring[q] = ~0ull;
-  for (int q = tid; q < 32; q += NT) hprog[q] = -1;
   __syncthreads();
   if (fused)
     for (int j = tid; j < u.nkey; j += NT) s_slot[s_kchar[j]] = static_cast<short>(j);
@@ -340,24 +349,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(max_threads_for<K>()
   };
 
   // ---- roles ----
-  // The SMSP warp arbiter favours the highest warp id (B300_MICROARCH.md), so
-  // the latency-critical chain warps take the highest ids: warp 0 = service,
-  // warps 1..NCW = helpers, warps NCW+1..2*NCW = chain. Chain warp c (c =
-  // 0..NCW-1) and its helper then sit on different SMSPs.
+  // Warp w runs on SM sub-partition (SMSP) w % 4 and the SMSP arbiter favours
+  // the highest warp id (B300_MICROARCH.md): the service warp is warp 0, the
+  // latency-critical chain warps are 1..NCW (three for English: one SMSP each).
   const bool service = warp == 0;
-  const bool is_helper = warp >= 1 && warp <= NCW && warp - 1 < nw_u;
-  const bool is_chain = warp > NCW && warp - NCW - 1 < nw_u;
-  const int cwarp = is_helper ? warp - 1 : (is_chain ? warp - NCW - 1 : 0);  // chain-warp index of the cells
-  const int ctid = cwarp * 32 + lane;                                       // chain thread index of those cells
+  const bool is_chain = warp >= 1 && warp - 1 < nw_u;
+  const int cwarp = is_chain ? warp - 1 : 0;  // chain-warp index
+  const int ctid = cwarp * 32 + lane;         // chain thread index
 
-  // Cells of this lane (chain and helper share the map).
+  // Cells of this lane.
   bool has_b[K], has_l[K];
 #pragma unroll
   for (int p = 0; p < K; ++p) {
     const int i = ctid * K + p;
     const int li = dir == 0 ? i : i - 1;  // label index of this pair's label cell
-    has_b[p] = (is_chain || is_helper) && i <= L;
-    has_l[p] = (is_chain || is_helper) && li >= 0 && li < L;
+    has_b[p] = is_chain && i <= L;
+    has_l[p] = is_chain && li >= 0 && li < L;
   }
 
   float Zh = 0.f, Zl = 0.f;
@@ -367,12 +374,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(max_threads_for<K>()
   // =====================================================================
   // Service warp: staging / emissions / statistics / gradient rows.
   // =====================================================================
+  // Flat (frame, symbol) loops over a whole epoch: idx -> (idx / nstage,
+  // idx % nstage) by a multiply-high with a rounded-up reciprocal (exact for
+  // idx < 2^16 and nstage < 2^16).
+  const unsigned recip = static_cast<unsigned>((0x100000000ull + nstage - 1) / nstage);
+  auto split_idx = [&](int idx, int& r, int& c) {
+    r = static_cast<int>(__umulhi(static_cast<unsigned>(idx), recip));
+    c = idx - r * nstage;
+  };
+  const float* xb_utt = a.x + static_cast<size_t>(b) * a.A;
   auto stage = [&](const Epoch& e) {
     if (e.phase == 0) return;
-    for (int k = e.k0; k < e.k1; ++k) {
-      const float* src = a.x + static_cast<size_t>(frame(k)) * rs + static_cast<size_t>(b) * a.A;
-      float* dst = xraw + (k & MX) * g.xstride;
-      for (int c = lane; c < nstage; c += 32) cp_async4(dst + c, src + (fused ? c : s_kchar[c]));
+    const int total = (e.k1 - e.k0) * nstage;
+#pragma unroll 4
+    for (int idx = lane; idx < total; idx += 32) {
+      int r, c;
+      split_idx(idx, r, c);
+      const int k = e.k0 + r;
+      cp_async4(xraw + (k & MX) * g.xstride + c,
+                xb_utt + static_cast<size_t>(frame(k)) * rs + (fused ? c : s_kchar[c]));
     }
     cp_async_commit();
   };
@@ -406,11 +426,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(max_threads_for<K>()
       lser[k & MX] = make_float2(mk, ls);
       if (k <= kcount) part_acc += fused ? static_cast<double>(ls) : -static_cast<double>(mk);
     }
+    if (lane < n) emis[((e.k0 + lane) & M2) * SW + g.SW] = make_float2(SENT, 0.f);
     __syncwarp();
-    for (int k = e.k0; k < e.k1; ++k) {
-      const float mk = lser[k & MX].x;
-      for (int c = lane; c < nstage; c += 32) emis[(k & M2) * SW + c] = emis_df(xraw[(k & MX) * g.xstride + c], mk);
-      if (lane == 0) emis[(k & M2) * SW + g.SW] = make_float2(SENT, 0.f);
+    const int total = n * nstage;
+#pragma unroll 4
+    for (int idx = lane; idx < total; idx += 32) {
+      int r, c;
+      split_idx(idx, r, c);
+      const int k = e.k0 + r;
+      emis[(k & M2) * SW + c] = emis_df(xraw[(k & MX) * g.xstride + c], lser[k & MX].x);
     }
   };
   // Gradient rows of a finished phase-2 epoch, lane = row (ctc.cpp:196-203,
@@ -476,22 +500,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(max_threads_for<K>()
       for (int j = 0; j < u.nkey; ++j) tr[j] = oc[j];
     }
     __syncwarp();
-    for (int r = 0; r < n; ++r) {
-      const int t = frame(e.k0 + r);
-      const float* trr = tile + r * g.tstride;
-      if (fused) {
-        float* gr = a.grad + static_cast<size_t>(t) * rs + static_cast<size_t>(b) * a.A;
-        for (int c = lane; c < a.A; c += 32) gr[c] = trr[c];
-      } else {
-        float* orow = a.occ + u.occ_off + static_cast<size_t>(t) * u.nkey;
-        for (int j = lane; j < u.nkey; j += 32) orow[j] = trr[j];
+    const int total = n * nstage;  // fused: nstage == A; split: nstage == nkey
+    if (fused) {
+      float* gb = a.grad + static_cast<size_t>(b) * a.A;
+#pragma unroll 4
+      for (int idx = lane; idx < total; idx += 32) {
+        int r, c;
+        split_idx(idx, r, c);
+        gb[static_cast<size_t>(frame(e.k0 + r)) * rs + c] = tile[r * g.tstride + c];
+      }
+    } else {
+      float* ob = a.occ + u.occ_off;
+#pragma unroll 4
+      for (int idx = lane; idx < total; idx += 32) {
+        int r, c;
+        split_idx(idx, r, c);
+        ob[static_cast<size_t>(frame(e.k0 + r)) * u.nkey + c] = tile[r * g.tstride + c];
       }
     }
     __syncwarp();
   };
 
   // =====================================================================
-  // Chain warps: the recursion only.
+  // Chain warps: the recursion, and one step behind it (same basic block,
+  // so the scheduler fills the recursion's latency gaps with it) the
+  // column's storage (phase 1) or occupancies (phase 2).
   // =====================================================================
   // Emission-row index of each cell; cells that do not exist read the
   // sentinel column (no predicate between the loads and their use).
@@ -504,9 +537,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(max_threads_for<K>()
     const int sym = has_l[p] ? s_lab[li] : a.blank;
     sidx_l[p] = has_l[p] ? (fused ? sym : s_slotpos[li]) : g.SW;
     sidx_b[p] = has_b[p] ? (fused ? a.blank : 0) : g.SW;
-    skip[p] = (is_chain || is_helper) && i >= 1 && i < L && s_lab[i] != a.blank && s_lab[i] != s_lab[i - 1];
+    skip[p] = is_chain && i >= 1 && i < L && s_lab[i] != a.blank && s_lab[i] != s_lab[i - 1];
   }
-  DF vb[K], vl[K];  // published values: alpha (forward) or emission-inclusive beta~ (backward)
+  DF vb[K], vl[K];  // carried values: alpha (forward) or emission-inclusive beta~ (backward)
   DF xb[K], xl[K];  // backward only: emission-exclusive beta (what storage / occupancy use)
   float2 eB[K], eL[K];
 #pragma unroll
@@ -514,9 +547,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(max_threads_for<K>()
     vb[p] = vl[p] = xb[p] = xl[p] = sent();
     eB[p] = eL[p] = make_float2(SENT, 0.f);
   }
-  unsigned long long* my_ring = hring + static_cast<size_t>(cwarp) * RH * 64 * K;
 
-  // Cells that do not exist get a sentinel emission (no predicate on the critical path).
   auto load_emis = [&](int k) {
     const float2* er = emis + (k & M2) * SW;
 #pragma unroll
@@ -543,260 +574,207 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(max_threads_for<K>()
     if (dir == 0) st_tagged(lane == 31 && cwarp + 1 < nw_u, bnd + cwarp * P2, vl[K - 1], 0);
     else st_tagged(lane == 0 && cwarp > 0, bnd + cwarp * P2, vl[0], 0);
   };
-  // Boundary value of the neighbouring warp, prefetched one step early
-  // (the neighbour normally runs >= 2 steps ahead); re-polled if stale.
+  // Neighbour value for step k: a shuffle inside the warp; across warps the
+  // tagged boundary slot, prefetched one step early (the upstream warp runs
+  // ahead: its boundary cell depends on the far side of the warp only K
+  // steps later), re-polled if stale.
   unsigned long long bpre = ~0ull;
-  auto take_boundary = [&](const unsigned long long* slot, int tag) -> DF {
-#ifdef DS2CTC_EXP_NOBND
-    return sent();
-#endif
-    unsigned long long u = bpre;
-    if ((u & 0xFFull) != (static_cast<unsigned long long>(tag) & 0xFFull)) return ld_tagged(slot, tag);
-    return tag_unpack(u);
-  };
-  auto prefetch_boundary = [&](const unsigned long long* slot) {
-#ifdef DS2CTC_EXP_NOBND
-    return;
-#endif
-    asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(bpre) : "r"(smem_addr(slot)));
-  };
-  auto critical = [&](int k) {  // k >= 1
+  auto neighbour = [&](int k) -> DF {
+    DF nb;
     if (dir == 0) {
-      DF nb;
       nb.h = __shfl_up_sync(0xffffffffu, vl[K - 1].h, 1);
       nb.l = __shfl_up_sync(0xffffffffu, vl[K - 1].l, 1);
-      if (cwarp > 0) {
-        const DF bv = take_boundary(bnd + (cwarp - 1) * P2 + ((k - 1) & M2), k - 1);
-        if (lane == 0) nb = bv;
-      } else if (lane == 0) {
-        nb = sent();
-      }
-      DF nvb[K], nvl[K];
-#pragma unroll
-      for (int p = 0; p < K; ++p) {
-        const DF n1 = p == 0 ? nb : vl[p - 1];
-        DF mb, ml;
-        const float cb = lse2(vb[p], n1, mb);                          // blank 2i <- 2i, 2i-1
-        const float cl = lse3(vl[p], vb[p], skip[p] ? n1 : sent(), ml);  // label 2i+1 <- 2i+1, 2i, 2i-1
-        nvb[p] = incl(mb, cb, eB[p]);
-        nvl[p] = incl(ml, cl, eL[p]);
-      }
-#pragma unroll
-      for (int p = 0; p < K; ++p) {
-        vb[p] = nvb[p];
-        vl[p] = nvl[p];
-      }
-      st_tagged(lane == 31 && cwarp + 1 < nw_u, bnd + cwarp * P2 + (k & M2), vl[K - 1], k);
-      if (cwarp > 0) prefetch_boundary(bnd + (cwarp - 1) * P2 + (k & M2));
     } else {
-      DF nb;
       nb.h = __shfl_down_sync(0xffffffffu, vl[0].h, 1);
       nb.l = __shfl_down_sync(0xffffffffu, vl[0].l, 1);
-      if (cwarp + 1 < nw_u) {
-        const DF bv = take_boundary(bnd + (cwarp + 1) * P2 + ((k - 1) & M2), k - 1);
-        if (lane == 31) nb = bv;
-      } else if (lane == 31) {
-        nb = sent();
+    }
+    const int up = dir == 0 ? cwarp - 1 : cwarp + 1;  // upstream warp
+    const bool edge_lane = lane == (dir == 0 ? 0 : 31);
+    if (up >= 0 && up < nw_u) {
+      unsigned long long v = bpre;
+      if ((v & 0xFFull) != (static_cast<unsigned long long>(k - 1) & 0xFFull)) {
+        const DF w = ld_tagged(bnd + up * P2 + ((k - 1) & M2), k - 1);
+        v = tag_pack(w, k - 1);
       }
-      DF nvb[K], nvl[K];
+      if (edge_lane) nb = tag_unpack(v);
+    } else if (edge_lane) {
+      nb = sent();
+    }
+    return nb;
+  };
+  auto step = [&](int k, DF nb) {  // column k from column k - 1, k >= 1
+    DF nvb[K], nvl[K];
 #pragma unroll
-      for (int p = K - 1; p >= 0; --p) {
-        const DF n1 = p == K - 1 ? nb : vl[p + 1];
-        DF mb, ml;
-        const float cb = lse2(vb[p], n1, mb);                          // blank 2i <- 2i, 2i+1
-        const float cl = lse3(vl[p], vb[p], skip[p] ? n1 : sent(), ml);  // label 2i-1 <- 2i-1, 2i, 2i+1
-        nvb[p] = incl(mb, cb, eB[p]);
-        nvl[p] = incl(ml, cl, eL[p]);
+    for (int q = 0; q < K; ++q) {
+      const int p = dir == 0 ? q : K - 1 - q;
+      const DF n1 = dir == 0 ? (p == 0 ? nb : vl[p - 1]) : (p == K - 1 ? nb : vl[p + 1]);
+      DF mb, ml;
+      const float cb = lse2(vb[p], n1, mb);                            // blank 2i <- 2i, 2i -+ 1
+      const float cl = lse3(vl[p], vb[p], skip[p] ? n1 : sent(), ml);  // label <- itself, blank 2i, 2i -+ 1
+      nvb[p] = incl(mb, cb, eB[p]);
+      nvl[p] = incl(ml, cl, eL[p]);
+      if (dir == 1) {
         xb[p] = excl(mb, cb);
         xl[p] = excl(ml, cl);
       }
-#pragma unroll
-      for (int p = 0; p < K; ++p) {
-        vb[p] = nvb[p];
-        vl[p] = nvl[p];
-      }
-      st_tagged(lane == 0 && cwarp > 0, bnd + cwarp * P2 + (k & M2), vl[0], k);
-      if (cwarp + 1 < nw_u) prefetch_boundary(bnd + (cwarp + 1) * P2 + (k & M2));
     }
-  };
-  // Publish column k to the helper ring (after the helper freed the slot).
-  auto publish = [&](int k) {
-#ifdef DS2CTC_EXP_NOHELPER
-    return;
-#endif
-    if (k >= RH)
-      for (unsigned n = 0; ld_volatile_int(hprog + cwarp) < k - RH; ++n) {
-        __nanosleep(32);
-        if (n == kSpinLimit) {
-          watchdog_fire(2, k);
-          break;
-        }
-      }
-    unsigned long long* slot = my_ring + (k & MH) * 64 * K;
 #pragma unroll
     for (int p = 0; p < K; ++p) {
-      st_tagged(true, slot + (2 * p) * 32 + lane, dir == 0 ? vb[p] : xb[p], k);
-      st_tagged(true, slot + (2 * p + 1) * 32 + lane, dir == 0 ? vl[p] : xl[p], k);
+      vb[p] = nvb[p];
+      vl[p] = nvl[p];
     }
-  };
-  auto chain_epoch = [&](const Epoch& e) {
-    load_emis(e.k0);
-    for (int k = e.k0; k < e.k1; ++k) {
-      STEP_STAMP(k, e, 0);
-      if (k == 0) first_column();
-      else if (e.phase == 1 || k > kmid) critical(k);
-      STEP_STAMP(k, e, 1);
-      if (k + 1 < e.k1) load_emis(k + 1);
-      publish(k);
-      STEP_STAMP(k, e, 2);
-    }
+    const int down = dir == 0 ? cwarp + 1 : cwarp - 1;
+    if (dir == 0) st_tagged(lane == 31 && down < nw_u, bnd + cwarp * P2 + (k & M2), vl[K - 1], k);
+    else st_tagged(lane == 0 && down >= 0, bnd + cwarp * P2 + (k & M2), vl[0], k);
+    const int up = dir == 0 ? cwarp - 1 : cwarp + 1;
+    if (up >= 0 && up < nw_u)
+      asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(bpre) : "r"(smem_addr(bnd + up * P2 + (k & M2))));
   };
 
-  // =====================================================================
-  // Helper warps: store (phase 1) / occupancy (phase 2) of published columns.
-  // =====================================================================
-  // Partner (offset, deltas) of this lane's cells for a phase-2 row, loaded
-  // straight from the (L2-resident) store two steps ahead of use.
-  struct PartnerRow {
-    float off_lo, off_hi;  // offsets of the writer threads of the lane's first / last slot
-    float d[2 * K];        // the partner's deltas for slots 2*ctid*K + pshift ... (+2K)
-  };
-  // The partner's slot of cell s is s + 1 when the partner is the backward CTA
-  // and s when it is the forward one; this lane's first cell is 2*ctid*K
-  // (forward: blank) or 2*ctid*K - 1 (backward: label), so its first partner
-  // slot is 2*ctid*K + 1 resp. 2*ctid*K - 1 (slot -1 belongs to no cell and
-  // is never used).
-  const int lane_slot0 = 2 * ctid * K + (dir == 0 ? 1 : -1);
-  auto load_partner = [&](int k, PartnerRow& r) {
-    if (k >= T || !is_helper || ctid * K > L) return;
-    const float* col = a.store + u.store_off + static_cast<size_t>(frame(k)) * cw;
-    const int s0 = lane_slot0;
+  // Phase 1: column k -> fp32 deltas from this thread's own max hi part (no
+  // cross-lane reduction). Sentinel cells need no special case: their deltas
+  // (or the offset itself) stay below -1e29 and give 2^gamma = 0.
+  auto store_column = [&](int k) {
+    DF cb[K], clv[K];  // static selects: a pointer to either register array would live in local memory
 #pragma unroll
-    for (int q = 0; q < 2 * K; ++q) r.d[q] = col[s0 + q];
-    r.off_lo = col[OB + s0 / (2 * K)];
-    r.off_hi = col[OB + (s0 + 2 * K - 1) / (2 * K)];
-  };
-  auto helper_epoch = [&](const Epoch& e) {
-    PartnerRow pa{}, pb{};
-    if (e.phase == 2) {
-      load_partner(e.k0, pa);
-      load_partner(e.k0 + 1, pb);
+    for (int p = 0; p < K; ++p) {
+      cb[p] = dir == 0 ? vb[p] : xb[p];
+      clv[p] = dir == 0 ? vl[p] : xl[p];
     }
-    for (int k = e.k0; k < e.k1; ++k) {
-      STEP_STAMP(k, e, 0);
-      const unsigned long long* slot = my_ring + (k & MH) * 64 * K;
-      // One round trip for all 2K values of this lane, then re-poll if any is stale.
-      unsigned long long raw[2 * K];
-      for (unsigned n = 0;; ++n) {
-        if (n == kSpinLimit) {
-          watchdog_fire(3, k);
-          break;
-        }
-        bool ok = true;
+    float hm = fmaxf(cb[0].h, clv[0].h);
 #pragma unroll
-        for (int q = 0; q < 2 * K; ++q) {
-          asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(raw[q]) : "r"(smem_addr(slot + q * 32 + lane)));
-          ok &= (raw[q] & 0xFFull) == (static_cast<unsigned long long>(k) & 0xFFull);
-        }
-        if (ok) break;
-        __nanosleep(32);
-      }
-      DF cb[K], clv[K];
+    for (int p = 1; p < K; ++p) hm = fmaxf(hm, fmaxf(cb[p].h, clv[p].h));
+    const int col = (dir == 0 && k == kmid) ? T : frame(k);
+    float* dst = a.store + u.store_off + static_cast<size_t>(col) * cw;
+    if (ctid < column_threads(L, K)) {
 #pragma unroll
       for (int p = 0; p < K; ++p) {
-        cb[p] = tag_unpack(raw[2 * p]);
-        clv[p] = tag_unpack(raw[2 * p + 1]);
+        const float db = (cb[p].h - hm) + cb[p].l;
+        const float dl = (clv[p].h - hm) + clv[p].l;
+        // forward pair = slots (blank 2i, label 2i+1); backward = (label 2i-1, blank 2i) at +1
+        reinterpret_cast<float2*>(dst)[ctid * K + p] = dir == 0 ? make_float2(db, dl) : make_float2(dl, db);
       }
-      __syncwarp();
-      if (lane == 0) st_volatile_int(hprog + cwarp, k);
-      STEP_STAMP(k, e, 1);
-      if (e.phase == 1) {
-        // fp32 deltas from this thread's own max hi part (no cross-lane
-        // reduction); sentinels are stored as -inf.
-        float hm = NEGF;
-#pragma unroll
-        for (int p = 0; p < K; ++p) {
-          if (cb[p].h > SENT_CUT) hm = fmaxf(hm, cb[p].h);
-          if (clv[p].h > SENT_CUT) hm = fmaxf(hm, clv[p].h);
-        }
-        const int col = (dir == 0 && k == kmid) ? T : frame(k);
-        float* dst = a.store + u.store_off + static_cast<size_t>(col) * cw;
-        if (ctid < column_threads(L, K)) {
-#pragma unroll
-          for (int p = 0; p < K; ++p) {
-            const float db = (has_b[p] && cb[p].h > SENT_CUT) ? (cb[p].h - hm) + cb[p].l : NEGF;
-            const float dl = (has_l[p] && clv[p].h > SENT_CUT) ? (clv[p].h - hm) + clv[p].l : NEGF;
-            // forward pair = slots (blank 2i, label 2i+1); backward = (label 2i-1, blank 2i) at +1
-            reinterpret_cast<float2*>(dst)[ctid * K + p] = dir == 0 ? make_float2(db, dl) : make_float2(dl, db);
-          }
-          dst[OB + ctid] = hm;
-        }
-      } else {
-        // gamma = alpha + beta - log Z (plain add, ctc.cpp:200) -> occupancy 2^gamma.
-        float* ebr = eb + (k & M2) * g.estride;
-        float* elr = el + (k & M2) * g.estride;
-        auto occ = [&](DF v, float woff, float delta) -> float {
-          const DF p = two_sum(v.h, -Zh);
-          const float q = p.h + woff;
-          const float gg = q + ((p.l + v.l) + (delta - Zl));
-          const float o = ex2(gg);
-          return (v.h <= SENT_CUT || woff == NEGF || delta == NEGF) ? 0.f : o;
-        };
-        // This lane's cells in slot order: forward (blank 2i, label 2i+1) at
-        // partner slots 2i+1, 2i+2; backward (label 2i-1, blank 2i) at 2i-1, 2i.
-        const int s0 = lane_slot0;
-#pragma unroll
-        for (int p = 0; p < K; ++p) {
-          const int i = ctid * K + p;
-          // static register indices only (a runtime index would spill the row to local memory)
-          const float d_even = pa.d[2 * p], d_odd = pa.d[2 * p + 1];
-          const int qb = dir == 0 ? 2 * p : 2 * p + 1;  // position of the blank cell among the lane's 2K cells
-          const int ql = dir == 0 ? 2 * p + 1 : 2 * p;
-          const float ob = (s0 + qb) / (2 * K) == s0 / (2 * K) ? pa.off_lo : pa.off_hi;
-          const float ol = (s0 + ql) / (2 * K) == s0 / (2 * K) ? pa.off_lo : pa.off_hi;
-          if (has_b[p]) ebr[i] = occ(cb[p], ob, dir == 0 ? d_even : d_odd);
-          if (has_l[p]) elr[dir == 0 ? i : i - 1] = occ(clv[p], ol, dir == 0 ? d_odd : d_even);
-        }
-        pa = pb;
-        load_partner(k + 2, pb);
-      }
-      STEP_STAMP(k, e, 2);
+      dst[OB + ctid] = hm;
     }
   };
 
-#ifdef DS2CTC_EXP_TIGHT
-  // Debug: the recursion alone, 1000 steps back to back on chain warp 0 (its
-  // neighbour value is the sentinel), timed with clock64.
-#ifdef DS2CTC_EXP_NOBND
-  if (blockIdx.x < 2 && is_chain && dir == 0) {  // all forward chain warps, no neighbour exchange
-#else
-  if (blockIdx.x < 2 && is_chain && cwarp == 0 && dir == 0) {  // forward chain warp 0 has no neighbour
-#endif
-    long long t0 = clock64();
-    for (int it = 0; it < 1000; ++it) critical(2 + (it & 1));
-    long long t1 = clock64();
-    if (lane == 0 && cwarp == 0) g_step_clock[dir][7][31][3] = t1 - t0;
-    t0 = clock64();
-    for (int it = 0; it < 1000; ++it) {
-      critical(2 + (it & 1));
-      load_emis(3 + (it & 7));
+  // Phase 2: the partner's stored cells of this warp, streamed by cp.async
+  // (16-byte chunks, shared by the warp) kPartnerDepth - 2 steps ahead into
+  // a ring of rows laid out as
+  //   [4: deltas below] [64K: deltas of the warp's slots] [4: deltas above]
+  //   [4: offsets below] [32: offsets of the warp's threads] [4: offsets above].
+  // The partner's slot of cell s is s + 1 when the partner is the backward
+  // CTA and s when it is the forward one: a forward lane's cells sit at
+  // partner slots 2*ctid*K + 1 .. 2*ctid*K + 2K (the last one may belong to
+  // the next warp), a backward lane's at 2*ctid*K - 1 .. 2*ctid*K + 2K - 2.
+  constexpr int PD = kPartnerDepth;
+  constexpr int ROW = 64 * K + 48;             // floats per warp row
+  constexpr int NCH = 16 * K + 10;             // 16-byte chunks per row actually fetched
+  constexpr int NIT = (NCH + 31) / 32;
+  float* prow0 = reinterpret_cast<float*>(smem + g.off_pring) + cwarp * ROW;
+  const int wbase = 64 * K * cwarp;            // first partner slot of this warp
+  int ch_src[NIT], ch_dst[NIT];
+  bool ch_on[NIT];
+#pragma unroll
+  for (int j = 0; j < NIT; ++j) {
+    const int c = lane + 32 * j;
+    int src, dst;
+    bool on;
+    if (c < 16 * K + 1) {  // forward: deltas + the chunk above; backward: the chunk below + deltas
+      const int q = dir == 0 ? c : c - 1;
+      src = wbase + 4 * q;
+      dst = 4 * (q + 1);
+      on = dir == 0 ? (q < 16 * K || cwarp + 1 < nw_u) : (q >= 0 || cwarp > 0);
+    } else {  // offsets: 9 chunks (the 8 of the warp + the one above or below)
+      const int q = (c - (16 * K + 1)) + (dir == 0 ? 0 : -1);
+      src = OB + 32 * cwarp + 4 * q;
+      dst = 64 * K + 8 + 4 * (q + 1);
+      on = c < NCH && (dir == 0 ? (q < 8 || cwarp + 1 < nw_u) : (q >= 0 || cwarp > 0));
     }
-    t1 = clock64();
-    if (lane == 0 && cwarp == 0) g_step_clock[dir][7][31][2] = t1 - t0;
-    t0 = clock64();
-    const Epoch fake{2, 1002, 1};
-    for (int k = 2; k < 1002; ++k) {
-      STEP_STAMP(k, fake, 0);
-      critical(k);
-      STEP_STAMP(k, fake, 1);
-      load_emis(k + 1);
-      STEP_STAMP(k, fake, 2);
-    }
-    t1 = clock64();
-    if (lane == 0 && cwarp == 0) g_step_clock[dir][7][31][1] = t1 - t0;
-    if (vl[0].h == 12345.f) a.costs[b] = vl[K - 1].l;  // keep the loop alive
+    ch_on[j] = is_chain && on && src + 4 <= cw;
+    ch_src[j] = src;
+    ch_dst[j] = dst;
   }
-#endif
+  const bool own_cells = is_chain && ctid * K <= L;
+  auto partner_prefetch = [&](int k) {
+    const float* col = a.store + u.store_off + static_cast<size_t>(frame(k)) * cw;
+    float* row = prow0 + (k & (PD - 1)) * NCW * ROW;
+#pragma unroll
+    for (int j = 0; j < NIT; ++j) cp_async16_if(ch_on[j] && k < T, row + ch_dst[j], col + ch_src[j]);
+    cp_async_commit();
+  };
+  // gamma = alpha + beta - log Z (plain add, ctc.cpp:200) -> occupancy 2^gamma.
+  // The carried values were shifted by -log Z at the meet, so gamma is one
+  // near-cancelling add of the partner's offset plus the small parts.
+  auto occupancy_column = [&](int k) {
+    cp_async_wait<PD - 2>();
+    __syncwarp();  // chunks were fetched by other lanes
+    const float* row = prow0 + (k & (PD - 1)) * NCW * ROW;
+    const int d0 = 2 * K * lane + (dir == 0 ? 5 : 3);
+    float d[2 * K];
+#pragma unroll
+    for (int q = 0; q < 2 * K; ++q) d[q] = row[d0 + q];
+    const float* offs = row + 64 * K + 12 + lane;
+    const float off_lo = dir == 0 ? offs[0] : offs[-1];
+    const float off_hi = dir == 0 ? offs[1] : offs[0];
+    float* ebr = eb + (k & M2) * g.estride;
+    float* elr = el + (k & M2) * g.estride;
+#pragma unroll
+    for (int p = 0; p < K; ++p) {
+      const int i = ctid * K + p;
+      const DF vbp = dir == 0 ? vb[p] : xb[p];
+      const DF vlp = dir == 0 ? vl[p] : xl[p];
+      // cell positions among the lane's 2K partner slots, and their writer thread
+      const int qb = dir == 0 ? 2 * p : 2 * p + 1;
+      const int ql = dir == 0 ? 2 * p + 1 : 2 * p;
+      const float ob = (dir == 0 ? qb == 2 * K - 1 : qb != 0) ? off_hi : off_lo;
+      const float ol = (dir == 0 ? ql == 2 * K - 1 : ql != 0) ? off_hi : off_lo;
+      const float o_b = ex2((vbp.h + ob) + (vbp.l + d[qb]));
+      const float o_l = ex2((vlp.h + ol) + (vlp.l + d[ql]));
+      if (has_b[p]) ebr[i] = o_b;
+      if (has_l[p]) elr[dir == 0 ? i : i - 1] = o_l;
+    }
+  };
+
+  // Steps [k0, k1) of one epoch. Step k computes column k and finishes
+  // column k - 1; the epoch's last column is finished after the loop.
+  bool partner_started = false;
+  auto chain_epoch = [&](const Epoch& e) {
+    const bool ph2 = e.phase == 2;
+    if (ph2 && !partner_started) {  // the partner stream is continuous across phase-2 epochs
+      partner_started = true;
+      for (int j = 0; j < PD - 2; ++j) partner_prefetch(e.k0 + j);
+    }
+    load_emis(e.k0);
+    STEP_STAMP(e.k0, e, 0);
+    if (!ph2 && e.k0 == 0) first_column();
+    else if (!ph2 || e.k0 > kmid) step(e.k0, neighbour(e.k0));  // the forward CTA's phase 2 starts at kmid
+    load_emis(e.k0 + 1);
+    if (ph2) partner_prefetch(e.k0 + PD - 2);
+    STEP_STAMP(e.k0, e, 2);
+    if (ph2) {
+      for (int k = e.k0 + 1; k < e.k1; ++k) {
+        STEP_STAMP(k, e, 0);
+        const DF nb = neighbour(k);
+        occupancy_column(k - 1);
+        step(k, nb);
+        load_emis(k + 1);
+        partner_prefetch(k + PD - 2);
+        STEP_STAMP(k, e, 2);
+      }
+      occupancy_column(e.k1 - 1);
+    } else {
+      for (int k = e.k0 + 1; k < e.k1; ++k) {
+        STEP_STAMP(k, e, 0);
+        const DF nb = neighbour(k);
+        store_column(k - 1);
+        step(k, nb);
+        load_emis(k + 1);
+        STEP_STAMP(k, e, 2);
+      }
+      store_column(e.k1 - 1);
+    }
+  };
   // ---- prologue staging of epoch 0 ----
   Epoch cur{0, min(P, kmid + 1), 1};
   if (service) {
@@ -823,18 +801,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(max_threads_for<K>()
     if (stg.phase != 0 && stg.k0 < cur.k1) stg.k0 = cur.k1;
     if (service) {
 #ifndef DS2CTC_EXP_NOSERVICE
+#ifdef DS2CTC_EPOCH_TIMING
+      const bool stamp = blockIdx.x < 2 && lane == 0 && epoch_idx < 32;
+      if (stamp) g_step_clock[dir][7][epoch_idx][0] = clock64();
+#endif
       stage(stg);
       grad_rows(prev);
+#ifdef DS2CTC_EPOCH_TIMING
+      if (stamp) g_step_clock[dir][7][epoch_idx][1] = clock64();
+#endif
       cp_async_wait_all();
       __syncwarp();
+#ifdef DS2CTC_EPOCH_TIMING
+      if (stamp) g_step_clock[dir][7][epoch_idx][2] = clock64();
+#endif
       convert(stg);
+#ifdef DS2CTC_EPOCH_TIMING
+      if (stamp) g_step_clock[dir][7][epoch_idx][3] = clock64();
+#endif
 #endif
     } else if (is_chain) {
       chain_epoch(cur);
-    } else if (is_helper) {
-#ifndef DS2CTC_EXP_NOHELPER
-      helper_epoch(cur);
-#endif
     }
 #ifdef DS2CTC_EPOCH_TIMING
     if (blockIdx.x < 2 && lane == 0 && epoch_idx < 128) g_epoch_clock[dir][epoch_idx][warp][1] = clock64();
@@ -853,10 +840,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(max_threads_for<K>()
       for (int s = tid; s < S; s += NT) {
         const float wa = ca[OB + s / (2 * K)], da = ca[s];                    // forward: slot s
         const float wb = cbp[OB + (s + 1) / (2 * K)], db = cbp[s + 1];        // backward: slot s + 1
-        if (wa == NEGF || da == NEGF || wb == NEGF || db == NEGF) continue;
         const double v = (static_cast<double>(wa) + static_cast<double>(da)) +
                          (static_cast<double>(wb) + static_cast<double>(db));
-        mloc = v > mloc ? v : mloc;
+        if (v > kSentCutD) mloc = v > mloc ? v : mloc;  // sentinel cells are -inf
       }
       for (int o = 16; o > 0; o >>= 1) {
         const double w = __shfl_xor_sync(0xffffffffu, mloc, o);
@@ -873,10 +859,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(max_threads_for<K>()
         for (int s = tid; s < S; s += NT) {
           const float wa = ca[OB + s / (2 * K)], da = ca[s];
           const float wb = cbp[OB + (s + 1) / (2 * K)], db = cbp[s + 1];
-          if (wa == NEGF || da == NEGF || wb == NEGF || db == NEGF) continue;
           const double v = (static_cast<double>(wa) + static_cast<double>(da)) +
                            (static_cast<double>(wb) + static_cast<double>(db));
-          sl += ex2(static_cast<float>(v - M));
+          if (v > kSentCutD) sl += ex2(static_cast<float>(v - M));
         }
         for (int o = 16; o > 0; o >>= 1) sl += __shfl_xor_sync(0xffffffffu, sl, o);
         if (lane == 0) red[32 + warp] = static_cast<double>(sl);
@@ -889,6 +874,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(max_threads_for<K>()
       Zl = static_cast<float>(logz2 - static_cast<double>(Zh));
       dead = logz2 == -__builtin_huge_val();  // zero-probability lattice (ctc.cpp:189-193)
       if (dead || !want_grad) break;
+      if (is_chain) {
+        // Shift the carried column by -log Z (the recursion is shift-invariant),
+        // so phase-2 occupancies need no large subtraction, and re-publish
+        // the boundary cell of step kmid with the shift applied.
+        auto shift = [&](DF v) -> DF {
+          const DF t = two_sum(v.h, -Zh);
+          const float lo = t.l + (v.l - Zl);
+          const float h = t.h + lo;
+          return {h, lo - (h - t.h)};
+        };
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+          vb[p] = shift(vb[p]);
+          vl[p] = shift(vl[p]);
+          xb[p] = shift(xb[p]);
+          xl[p] = shift(xl[p]);
+        }
+        if (dir == 0) st_tagged(lane == 31 && cwarp + 1 < nw_u, bnd + cwarp * P2 + (kmid & M2), vl[K - 1], kmid);
+        else st_tagged(lane == 0 && cwarp > 0, bnd + cwarp * P2 + (kmid & M2), vl[0], kmid);
+        bpre = ~0ull;
+      }
       __syncthreads();
     }
     prev = cur;
@@ -916,8 +922,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(max_threads_for<K>()
 }
 
 template <int K>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(max_threads_for<K>(), 1) k_pair(PairArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  if (cluster_rank() == 0) pair_body<K, 0>(a, smem);
+  else pair_body<K, 1>(a, smem);
+}
+
+template <int K>
 int launch_k(const PairArgs& a, void* stream) {
-  const int threads = 32 * (2 * a.g.nchain + 1);
+  const int threads = 32 * (a.g.nchain + 1);
   if (threads > max_threads_for<K>()) return cudaErrorInvalidValue;
   cudaError_t err = cudaFuncSetAttribute(k_pair<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, a.g.smem);
   if (err != cudaSuccess) return err;

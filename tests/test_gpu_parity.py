@@ -52,7 +52,8 @@ def assert_parity(costs, grads, ref_costs, ref_grads, il, what):
         else:
             rel_max = 0.0
         print(f"PARITY {what}: max rel cost err {rel_max:.3e}, max abs grad err {err.max():.3e}")
-        assert err.max() <= GRAD_ATOL, f"{what}: grad abs err {err.max():.3e}"
+        worst = np.unravel_index(int(np.argmax(err)), err.shape)
+        assert err.max() <= GRAD_ATOL, f"{what}: grad abs err {err.max():.3e} at (t, b, c) = {worst}"
         for b in np.where(inf_ref)[0]:
             assert np.all(grads[:, b, :] == 0), f"{what}: infeasible utterance {b} has nonzero gradient"
         for b in range(len(il)):

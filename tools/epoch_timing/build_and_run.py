@@ -73,14 +73,19 @@ def run(so, A=29, T=700, L=150, B=64, brief=False):
             p2 = [r for r in rows[-8:-1]]
             busy2 = np.mean([[int(r[w, 1] - r[w, 0]) for w in range(8)] for r in p2], axis=0)
             print(f"  cta{cta}: phase-2 epoch busy per warp {busy2.astype(int).tolist()}")
+            sv = steps[cta, 7]
+            for ep in (2, len(rows) - 3):
+                if 0 < ep < 32 and sv[ep, 0] > 0:
+                    print(f"  cta{cta}: service epoch {ep}: stage+grad_rows {sv[ep,1]-sv[ep,0]}, wait {sv[ep,2]-sv[ep,1]}, convert {sv[ep,3]-sv[ep,2]}")
             busy = np.mean([[int(r[w, 1] - r[w, 0]) for w in range(8)] for r in p1], axis=0)
-            # chain warp 0 = warp NCW+1; per-step cycles over epoch 1 from the step stamps
-            w = 4
-            st = steps[cta, w]
-            n = int((st[:, 0] > 0).sum())
-            per = (st[n - 1, 0] - st[0, 0]) / max(n - 1, 1) if n > 1 else 0
-            crit = np.mean(st[:n, 1] - st[:n, 0]) if n else 0
-            print(f"  cta{cta}: chain-warp0 cycles/step {per:.0f} (critical {crit:.0f})")
+            # service = warp 0, chain warps 1..NCW; per-step cycles over the stamped phase-2 epoch
+            for w in (1, 2, 3):
+                st = steps[cta, w]
+                n = int((st[:, 0] > 0).sum())
+                if n > 1:
+                    per = (st[n - 1, 0] - st[0, 0]) / (n - 1)
+                    print(f"  cta{cta}: chain warp {w} phase-2 cycles/step {per:.0f}, "
+                          f"step body {np.mean(st[1:n, 2] - st[1:n, 0]):.0f}")
             total = int(rows[-1][0, 1] - rows[0][0, 0])
             print(f"  cta{cta}: total {total} cycles, phase-1 epoch busy per warp {busy.astype(int).tolist()}")
         return
