@@ -26,8 +26,7 @@ namespace ds2ctc {
 
 constexpr int kMaxStates = 4095;  // == DS2CTC_MAX_STATES
 constexpr int kFusedMaxAlphabet = 128;
-constexpr int kMaxThreads = 288;  // <= 8 chain warps (K = 8, L <= 2047) + 1 service warp
-constexpr int kPartnerDepth = 8;  // phase-2 partner rows in flight per chain thread (power of two)
+constexpr int kMaxThreads = 320;  // <= 8 chain warps (K = 8, L <= 2047) + service + gradient warps
 constexpr size_t kAlign = 256;
 constexpr size_t kSmemBudget = 220 * 1024;
 
@@ -60,7 +59,8 @@ struct Geometry {
   int fused;
   // shared-memory carve-up (bytes, 16-aligned)
   int off_xraw, off_emis, off_lse, off_eb, off_el, off_tile, off_occ, off_bnd, off_meta, off_red;
-  int off_pring;  // phase-2 partner rows: [kPartnerDepth][nchain][64K + 48] floats
+  int off_cb;     // column buffer [2][P][cw_max] floats (TMA bulk stores / loads of lattice columns)
+  int off_mbar;   // two mbarriers (one per column-buffer half)
   int xstride;    // floats per xraw row (odd)
   int estride;    // floats per eb/el row (odd)
   int cw_max;     // floats per stored column (max over batch)
@@ -120,7 +120,8 @@ inline Geometry make_geometry(int max_L_all, int max_L, int max_nkey, int A, boo
     g.off_tile = take(4 * 32 * g.tstride);  // one row per service lane (all 32 lanes run, P <= 32)
     g.off_occ = take(4 * 32 * g.ostride);
     g.off_bnd = take(8 * g.nchain * 2 * P);
-    g.off_pring = take(4 * kPartnerDepth * g.nchain * (64 * g.K + 48));
+    g.off_cb = take(4 * 2 * P * g.cw_max);
+    g.off_mbar = take(16);
     // meta: labels (L+1), key_char (nkey), key_start (nkey+1), key_pos (L), slot of each label
     // position (L+1), symbol -> slot (A shorts, fused)
     g.off_meta = take(4 * (4 * max_L + 2 * max_nkey + 8) + (fused ? 2 * A : 0));

@@ -17,6 +17,9 @@ def build(defines=()):
     os.makedirs(OUT, exist_ok=True)
     tag = "_".join(d.lower() for d in defines) or "base"
     so = os.path.join(OUT, f"libds2ctc_timing_{tag}.so")
+    srcs = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+    if os.path.exists(so) and all(os.path.getmtime(f) <= os.path.getmtime(so) for f in srcs):
+        return so  # prebuilt (e.g. shipped with the snapshot)
     objs = []
     for src in ("ctc_pair.cu", "ctc_dense.cu"):
         obj = os.path.join(OUT, tag + src + ".o")
@@ -103,7 +106,8 @@ def run(so, A=29, T=700, L=150, B=64, brief=False):
 
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "variants":
-        for defs in [()]:
+        sets = [tuple(v.split("+")) if v != "base" else () for v in sys.argv[2:]] or [()]
+        for defs in sets:
             so = build(defs)
             print("variant", defs or "base")
             run(so, brief=True)
