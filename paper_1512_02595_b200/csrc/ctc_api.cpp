@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <numeric>
@@ -15,6 +16,16 @@
 
 #include "ds2ctc.h"
 #include "ds2ctc_internal.h"
+
+namespace ds2ctc {
+int k1_max_pairs() {
+  static const int v = [] {
+    const char* e = std::getenv("DS2CTC_K1_MAX_PAIRS");
+    return e ? std::atoi(e) : 96;
+  }();
+  return v;
+}
+}  // namespace ds2ctc
 
 namespace ds2ctc {
 namespace {
@@ -124,8 +135,8 @@ ds2ctc_status validate(const int* label_lengths, const int* input_lengths, int A
 // Builds the metadata blob (int32 words laid out per Layout) into `blob`.
 // Returns (max L, max nkey) over utterances that run the lattice.
 std::pair<int, int> build_metadata(const Layout& lay, const int* flat_labels, const int* label_lengths,
-                                   const int* input_lengths, int B, int blank, std::vector<int32_t>& blob) {
-  blob.assign(lay.meta_end / sizeof(int32_t), 0);
+                                   const int* input_lengths, int A, int B, int blank, std::vector<int32_t>& blob) {
+  blob.resize(lay.meta_end / sizeof(int32_t));  // every word below is written
   auto* desc = reinterpret_cast<UttDesc*>(blob.data() + lay.desc / 4);
   int* order = blob.data() + lay.order / 4;
   int* labels = blob.data() + lay.labels / 4;
@@ -134,12 +145,23 @@ std::pair<int, int> build_metadata(const Layout& lay, const int* flat_labels, co
   int* key_pos = blob.data() + lay.key_pos / 4;
   if (lay.sum_L > 0) std::memcpy(labels, flat_labels, sizeof(int) * lay.sum_L);
 
+  // Per-symbol scratch, reset lazily by a per-utterance stamp (no O(A) clear per utterance).
+  thread_local std::vector<unsigned> stamp;
+  thread_local std::vector<int> cnt, next;
+  thread_local unsigned epoch = 0;
+  if (static_cast<int>(stamp.size()) < A) {
+    stamp.assign(A, 0u);
+    cnt.assign(A, 0);
+    next.assign(A, 0);
+  }
+  std::vector<int> distinct;
+  distinct.reserve(256);
+
   int max_L_all = 0;
   for (int b = 0; b < B; ++b) max_L_all = std::max(max_L_all, label_lengths[b]);
   const int K = pick_K(max_L_all);
   long long lab_off = 0, key_off = 0, store_off = 0, occ_off = 0;
   int max_L = 0, max_nkey = 1;
-  std::vector<std::pair<int, int>> kv;
   for (int b = 0; b < B; ++b) {
     UttDesc& u = desc[b];
     const int T = input_lengths[b], L = label_lengths[b];
@@ -154,27 +176,54 @@ std::pair<int, int> build_metadata(const Layout& lay, const int* flat_labels, co
     u.store_off = store_off;
     u.occ_off = occ_off;
     u.tm = T > 0 ? (T - 1) / 2 : 0;
+    u.pad0 = u.pad1 = u.pad2 = 0;
     // Key groups (group_rows_by_key, ctc.cpp:47-66) over label positions:
     // slot 0 = blank (all even lattice rows, plus label positions whose symbol
     // is the blank id), slots 1.. = distinct non-blank symbols ascending,
-    // positions ascending within a slot.
-    kv.clear();
-    for (int i = 0; i < L; ++i) kv.emplace_back(lab[i] == blank ? -1 : lab[i], i);
-    std::sort(kv.begin(), kv.end());
-    int nkey = 1;
-    key_char[key_off] = blank;
-    int* ks = key_start + key_off + b;
-    ks[0] = 0;
-    int r = 0;
-    size_t i = 0;
-    while (i < kv.size() && kv[i].first == -1) key_pos[lab_off + r++] = kv[i++].second;
-    ks[1] = r;
-    while (i < kv.size()) {
-      const int sym = kv[i].first;
-      key_char[key_off + nkey] = sym;
-      while (i < kv.size() && kv[i].first == sym) key_pos[lab_off + r++] = kv[i++].second;
-      ks[++nkey] = r;
+    // positions ascending within a slot. Counting sort by symbol.
+    if (++epoch == 0) {  // stamp wrap-around: clear once every 2^32 utterances
+      std::fill(stamp.begin(), stamp.end(), 0u);
+      epoch = 1;
     }
+    distinct.clear();
+    int n_blank = 0;
+    for (int i = 0; i < L; ++i) {
+      const int sym = lab[i];
+      if (sym == blank) {
+        ++n_blank;
+        continue;
+      }
+      if (stamp[sym] != epoch) {
+        stamp[sym] = epoch;
+        cnt[sym] = 0;
+        distinct.push_back(sym);
+      }
+      ++cnt[sym];
+    }
+    std::sort(distinct.begin(), distinct.end());
+    const int nkey = 1 + static_cast<int>(distinct.size());
+    int* ks = key_start + key_off + b;
+    key_char[key_off] = blank;
+    ks[0] = 0;
+    ks[1] = n_blank;
+    int run = n_blank;
+    for (int j = 0; j < nkey - 1; ++j) {
+      const int sym = distinct[j];
+      key_char[key_off + 1 + j] = sym;
+      next[sym] = run;
+      run += cnt[sym];
+      ks[2 + j] = run;
+    }
+    int* kp = key_pos + lab_off;
+    int nb = 0;
+    for (int i = 0; i < L; ++i) {
+      const int sym = lab[i];
+      if (sym == blank) kp[nb++] = i;
+      else kp[next[sym]++] = i;
+    }
+    // unused tail of this utterance's key CSR slots (nkey <= L + 1)
+    for (int j = nkey; j < L + 1; ++j) key_char[key_off + j] = 0;
+    for (int j = nkey + 1; j < L + 2; ++j) ks[j] = run;
     u.nkey = nkey;
     if (u.status == 0) {
       max_L = std::max(max_L, L);
@@ -208,7 +257,7 @@ ds2ctc_status run(const float* acts, float* grads, const int* flat_labels, const
   if (reinterpret_cast<uintptr_t>(workspace) % kAlign != 0) return DS2CTC_STATUS_INVALID_VALUE;
 
   thread_local std::vector<int32_t> blob;
-  const auto mx = build_metadata(lay, flat_labels, label_lengths, input_lengths, B, blank, blob);
+  const auto mx = build_metadata(lay, flat_labels, label_lengths, input_lengths, A, B, blank, blob);
 
   auto* ws = static_cast<unsigned char*>(workspace);
   auto s = static_cast<cudaStream_t>(stream);

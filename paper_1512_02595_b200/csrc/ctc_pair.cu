@@ -290,7 +290,7 @@ struct Epoch {
 // longer than 384) may use up to eight.
 template <int K>
 constexpr int max_threads_for() {
-  return K <= 4 ? 32 * 5 : kMaxThreads;
+  return K == 1 ? 32 * 8 : K <= 4 ? 32 * 5 : kMaxThreads;
 }
 
 // DIR 0: alpha forward (cluster rank 0), 1: beta backward (rank 1); a
@@ -997,8 +997,16 @@ template <int K>
 int launch_k(const PairArgs& a, void* stream) {
   const int threads = 32 * (a.g.nchain + 2);
   if (threads > max_threads_for<K>()) return cudaErrorInvalidValue;
-  cudaError_t err = cudaFuncSetAttribute(k_pair<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, a.g.smem);
-  if (err != cudaSuccess) return err;
+  // The dynamic shared-memory opt-in is set once per (device, K) to the budget.
+  static int configured[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !configured[dev]) {
+    cudaError_t err = cudaFuncSetAttribute(k_pair<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(kSmemBudget));
+    if (err != cudaSuccess) return err;
+    if (dev >= 0 && dev < 64) configured[dev] = 1;
+  }
   k_pair<K><<<2 * a.B, threads, a.g.smem, static_cast<cudaStream_t>(stream)>>>(a);
   return cudaGetLastError();
 }

@@ -75,8 +75,10 @@ DS2CTC_HD inline int chain_warps_for(int L, int K) { return (L + 1 + 32 * K - 1)
 // the service warp keeps an SM sub-partition (SMSP) of its own; each pair
 // costs 5 MUFU ops per step, so K also bounds the per-SMSP MUFU load.
 constexpr int kPairChoices[] = {1, 2, 3, 4, 6, 8};
+int k1_max_pairs();  // ctc_api.cpp (tunable: DS2CTC_K1_MAX_PAIRS)
 inline int pick_K(int max_L) {
   const int pairs = max_L + 1;
+  if (pairs <= k1_max_pairs()) return 1;
   for (int K : kPairChoices)
     if (pairs <= 96 * K) return K;
   return 8;
