@@ -75,8 +75,6 @@ __device__ __forceinline__ float block_sum(float v, float* sh) {
 
 __global__ void __launch_bounds__(kDenseThreads) k_dense(PairArgs a, int write_grad) {
   __shared__ float sh[32];
-  __shared__ unsigned bits[kDenseVec * kDenseThreads * 4 / 32];
-  __shared__ int nkey_s;
   const int row = blockIdx.x;
   const int t = row / a.B;
   const int b = row - t * a.B;
@@ -91,19 +89,13 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense(PairArgs a, int write_g
       for (int c = tid; c < A; c += kDenseThreads) gr[c] = 0.f;
     return;
   }
-  const int* keys = a.key_char + u.key_off;
-  const float* occ = a.occ + u.occ_off + static_cast<size_t>(t) * u.nkey;
   const bool vec = (A & 3) == 0 && A <= kDenseVec * kDenseThreads * 4;
-  if (gr && vec) {
-    for (int w = tid; w < (A + 31) / 32; w += kDenseThreads) bits[w] = 0u;
-    __syncthreads();
-    for (int j = tid; j < u.nkey; j += kDenseThreads) atomicOr(&bits[keys[j] >> 5], 1u << (keys[j] & 31));
-  }
-  if (vec) {
+  float m, ls;
+  if (vec) {  // the row stays in registers: one HBM read, one HBM write
     const int n4 = A >> 2;
     const float4* x4 = reinterpret_cast<const float4*>(xr);
     float4 v[kDenseVec];
-    float m = -__builtin_huge_valf();
+    m = -__builtin_huge_valf();
 #pragma unroll
     for (int j = 0; j < kDenseVec; ++j) {
       const int q = tid + j * kDenseThreads;
@@ -113,47 +105,45 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense(PairArgs a, int write_g
     m = block_max(m, sh);
     float s = 0.f;
 #pragma unroll
-    for (int j = 0; j < kDenseVec; ++j) {
-      const int q = tid + j * kDenseThreads;
-      if (q < n4) s += (__expf(v[j].x - m) + __expf(v[j].y - m)) + (__expf(v[j].z - m) + __expf(v[j].w - m));
-    }
+    for (int j = 0; j < kDenseVec; ++j)
+      s += (__expf(v[j].x - m) + __expf(v[j].y - m)) + (__expf(v[j].z - m) + __expf(v[j].w - m));
     s = block_sum(s, sh);
-    const float ls = logf(s);
-    if (tid == 0) a.lse[row] = make_float2(m, ls);
-    if (!gr) return;
-    float4* g4 = reinterpret_cast<float4*>(gr);
+    ls = logf(s);
+    if (gr) {
+      float4* g4 = reinterpret_cast<float4*>(gr);
+      const float off = m + ls;
 #pragma unroll
-    for (int j = 0; j < kDenseVec; ++j) {
-      const int q = tid + j * kDenseThreads;
-      if (q >= n4) continue;
-      float o[4] = {expf((v[j].x - m) - ls), expf((v[j].y - m) - ls), expf((v[j].z - m) - ls),
-                    expf((v[j].w - m) - ls)};
-      const unsigned word = bits[(4 * q) >> 5] >> ((4 * q) & 31);
-      if (word & 0xFu) {
-        for (int e = 0; e < 4; ++e) {
-          if (!((word >> e) & 1u)) continue;
-          const int c = 4 * q + e;
-          for (int j2 = 0; j2 < u.nkey; ++j2)
-            if (keys[j2] == c) o[e] -= occ[j2];
-        }
+      for (int j = 0; j < kDenseVec; ++j) {
+        const int q = tid + j * kDenseThreads;
+        if (q < n4)
+          stg_stream(g4 + q, make_float4(__expf(v[j].x - off), __expf(v[j].y - off), __expf(v[j].z - off),
+                                         __expf(v[j].w - off)));
       }
-      stg_stream(g4 + q, make_float4(o[0], o[1], o[2], o[3]));
     }
   } else {  // generic: two passes (the second hits L1/L2)
-    float m = -__builtin_huge_valf();
+    m = -__builtin_huge_valf();
     for (int c = tid; c < A; c += kDenseThreads) m = fmaxf(m, __ldg(xr + c));
     m = block_max(m, sh);
     float s = 0.f;
     for (int c = tid; c < A; c += kDenseThreads) s += __expf(__ldg(xr + c) - m);
     s = block_sum(s, sh);
-    const float ls = logf(s);
-    if (tid == 0) a.lse[row] = make_float2(m, ls);
-    if (!gr) return;
-    for (int c = tid; c < A; c += kDenseThreads) gr[c] = expf((__ldg(xr + c) - m) - ls);
-    __syncthreads();
-    for (int j = tid; j < u.nkey; j += kDenseThreads) gr[keys[j]] -= occ[j];
+    ls = logf(s);
+    if (gr)
+      for (int c = tid; c < A; c += kDenseThreads) gr[c] = __expf(__ldg(xr + c) - (m + ls));
   }
-  (void)nkey_s;
+  if (tid == 0) a.lse[row] = make_float2(m, ls);
+  if (!gr) return;
+  // Occupancy of the utterance's key symbols (<= L + 1 distinct symbols per
+  // row, the key map of group_rows_by_key, ctc.cpp:47-66): read-modify-write
+  // of the row just written (visible to the block after the barrier; the
+  // streaming stores did not allocate in L1, so these loads see them).
+  __syncthreads();
+  const int* keys = a.key_char + u.key_off;
+  const float* occ = a.occ + u.occ_off + static_cast<size_t>(t) * u.nkey;
+  for (int j = tid; j < u.nkey; j += kDenseThreads) {
+    const int c = keys[j];
+    gr[c] = gr[c] - occ[j];
+  }
 }
 
 // costs[b] = sum_t lse_t - log Z (natural log), one warp per utterance.
