@@ -48,19 +48,12 @@ namespace ds2ctc {
 namespace {
 
 constexpr float kL2eH = 1.44269502162933349609375f;  // fp32(log2 e)
-constexpr float kL2eL = 1.925963033500011e-08f;      // log2 e - kL2eH
 constexpr float kLn2f = 0.693147180559945309f;
 constexpr double kLn2 = 0.69314718055994530942;
 constexpr float NEGF = -__builtin_huge_valf();
 constexpr float SENT = -1e30f;     // "-inf" inside the recursion
 constexpr float SENT_CUT = -1e29f;  // below this a value is -inf
 constexpr double kSentCutD = -1e29;
-
-struct DF {
-  float h, l;
-};
-
-__device__ __forceinline__ DF sent() { return {SENT, 0.f}; }
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -74,51 +67,23 @@ __device__ __forceinline__ float lg2(float x) {
   return y;
 }
 
-__device__ __forceinline__ DF two_sum(float a, float b) {
-  const float s = a + b;
-  const float bb = s - a;
-  return {s, (a - (s - bb)) + (b - bb)};
-}
-
-// (x - mk) * log2(e) as an exact-to-fp32^2 double-float; -inf -> sentinel.
-__device__ __forceinline__ float2 emis_df(float x, float mk) {
-  const DF d = two_sum(x, -mk);
-  const float h = d.h * kL2eH;
-  const float l = fmaf(d.h, kL2eH, -h) + (d.h * kL2eL + d.l * kL2eH);
-  return x == NEGF ? make_float2(SENT, 0.f) : make_float2(h, l);
+// (x - mk) * log2(e), the shifted emission in log2 units; -inf -> sentinel.
+__device__ __forceinline__ float emis_log2(float x, float mk) {
+  return x == NEGF ? SENT : (x - mk) * kL2eH;
 }
 
 // Sorted log-sum-exp (log_sum_exp_guarded, ctc.hpp:30-35, in log2 units):
-// result = base + c with base the largest operand (exact double-float) and
-// c = lg2(1 + sum 2^(other - base)), the differences taken as double-floats.
-__device__ __forceinline__ float lse2(DF a, DF b, DF& base) {
-  const float d = (a.h - b.h) + (a.l - b.l);
-  base = d >= 0.f ? a : b;
-  return lg2(1.f + ex2(-fabsf(d)));
+// the largest operand plus lg2(1 + sum 2^(other - largest)); sentinels give
+// 2^(-huge) = 0, so no -inf guards are needed.
+__device__ __forceinline__ float lse2f(float a, float b) {
+  return fmaxf(a, b) + lg2(1.f + ex2(-fabsf(a - b)));
 }
 
-__device__ __forceinline__ float lse3(DF a, DF b, DF c, DF& base) {
-  const float d1 = (a.h - b.h) + (a.l - b.l);
-  const DF hi = d1 >= 0.f ? a : b;
-  const float d2 = (hi.h - c.h) + (hi.l - c.l);
-  base = d2 >= 0.f ? hi : c;
-  return lg2((1.f + ex2(fminf(d2, 0.f) - fabsf(d1))) + ex2(-fabsf(d2)));
-}
-
-// base + c + e, renormalised (Fast2Sum: |base| >= |e| except within the
-// first few frames, where both are small).
-__device__ __forceinline__ DF incl(DF m, float c, float2 e) {
-  const float s = m.h + e.x;
-  const float err = e.x - (s - m.h);
-  const float lo = ((m.l + e.y) + err) + c;
-  const float h = s + lo;
-  return {h, lo - (h - s)};
-}
-
-__device__ __forceinline__ DF excl(DF m, float c) {
-  const float lo = m.l + c;
-  const float h = m.h + lo;
-  return {h, lo - (h - m.h)};
+__device__ __forceinline__ float lse3f(float a, float b, float c) {
+  const float hi = fmaxf(a, b);
+  const float d1 = a - b;
+  const float d2 = hi - c;
+  return fmaxf(hi, c) + lg2((1.f + ex2(fminf(d2, 0.f) - fabsf(d1))) + ex2(-fabsf(d2)));
 }
 
 __device__ __forceinline__ void cluster_barrier() {
@@ -193,24 +158,23 @@ __device__ __forceinline__ void cp_async_wait() {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-// Tagged values: (hi, lo) with the step's low 8 bits in the lo mantissa (a
-// 2^-16 relative perturbation of lo, i.e. ~2^-40 of the value). An aligned
-// 64-bit shared store is single-copy atomic, so a reader that sees the tag
-// sees the value.
-__device__ __forceinline__ unsigned long long tag_pack(DF v, int tag) {
-  const unsigned lo = (__float_as_uint(v.l) & ~0xFFu) | (static_cast<unsigned>(tag) & 0xFFu);
-  return (static_cast<unsigned long long>(__float_as_uint(v.h)) << 32) | lo;
+// Tagged boundary values: residual r (32 bits) | offset O as a 24-bit
+// integer | the step's low 8 bits. An aligned 64-bit shared store is
+// single-copy atomic, so a reader that sees the tag sees the value.
+__device__ __forceinline__ unsigned long long tag_pack(float r, float o, int tag) {
+  const unsigned lo = (static_cast<unsigned>(__float2int_rn(o)) << 8) | (static_cast<unsigned>(tag) & 0xFFu);
+  return (static_cast<unsigned long long>(__float_as_uint(r)) << 32) | lo;
+}
+__device__ __forceinline__ float tag_r(unsigned long long u) { return __uint_as_float(static_cast<unsigned>(u >> 32)); }
+__device__ __forceinline__ float tag_o(unsigned long long u) {
+  return static_cast<float>(static_cast<int>(static_cast<unsigned>(u)) >> 8);
 }
 
-__device__ __forceinline__ DF tag_unpack(unsigned long long u) {
-  return {__uint_as_float(static_cast<unsigned>(u >> 32)), __uint_as_float(static_cast<unsigned>(u) & ~0xFFu)};
-}
-
-__device__ __forceinline__ void st_tagged(bool pred, unsigned long long* slot, DF v, int tag) {
+__device__ __forceinline__ void st_tagged(bool pred, unsigned long long* slot, float r, float o, int tag) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.volatile.shared.u64 [%0], %1;\n\t}" ::"r"(
           smem_addr(slot)),
-      "l"(tag_pack(v, tag)), "r"(static_cast<unsigned>(pred)));
+      "l"(tag_pack(r, o, tag)), "r"(static_cast<unsigned>(pred)));
 }
 
 // Watchdog: every spin-wait is bounded. A wait that exceeds the bound (a
@@ -231,19 +195,18 @@ __device__ __noinline__ void watchdog_fire(int kind, int step) {
 // Spin until the slot carries `tag`. Called warp-uniformly where possible.
 // Polls off the critical path back off with nanosleep so that spinning warps
 // do not crowd the shared-memory/shuffle (MIO) queue the recursion uses.
-template <bool kBackoff = false>
-__device__ __forceinline__ DF ld_tagged(const unsigned long long* slot, int tag, int kind = 1) {
+// Spin until the slot carries `tag`; returns the raw tagged word.
+__device__ __forceinline__ unsigned long long ld_tagged(const unsigned long long* slot, int tag, int kind = 1) {
   unsigned long long u;
   for (unsigned n = 0;; ++n) {
     asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(u) : "r"(smem_addr(slot)));
     if ((u & 0xFFull) == (static_cast<unsigned long long>(tag) & 0xFFull)) break;
-    if (kBackoff) __nanosleep(32);
     if (n == kSpinLimit) {
       watchdog_fire(kind, tag);
       break;
     }
   }
-  return tag_unpack(u);
+  return u;
 }
 
 // Wait for phase `parity` of an mbarrier (bounded, like every wait here).
@@ -340,7 +303,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   const int kcount = dir == 0 ? kmid : kmid - 1;  // steps whose frame this CTA adds to the cost
 
   float* xraw = reinterpret_cast<float*>(smem + g.off_xraw);
-  float2* emis = reinterpret_cast<float2*>(smem + g.off_emis);
+  float* emis = reinterpret_cast<float*>(smem + g.off_emis);
   float2* lser = reinterpret_cast<float2*>(smem + g.off_lse);
   float* eb = reinterpret_cast<float*>(smem + g.off_eb);
   float* el = reinterpret_cast<float*>(smem + g.off_el);
@@ -421,7 +384,6 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     has_l[p] = is_chain && li >= 0 && li < L;
   }
 
-  float Zh = 0.f, Zl = 0.f;
   double logz2 = 0.0;
   double part_acc = 0.0;  // service warp lanes: fused sum ls_t, split -sum mk_t (counted frames)
 
@@ -498,7 +460,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
       lser[k & MX] = make_float2(mk, ls);
       if (k <= kcount) part_acc += fused ? static_cast<double>(ls) : -static_cast<double>(mk);
     }
-    if (lane < n) emis[((e.k0 + lane) & M2) * SW + g.SW] = make_float2(SENT, 0.f);
+    if (lane < n) emis[((e.k0 + lane) & M2) * SW + g.SW] = SENT;
     __syncwarp();
     const int total = n * nstage;
 #pragma unroll 4
@@ -506,7 +468,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
       int r, c;
       split_idx(idx, r, c);
       const int k = e.k0 + r;
-      emis[(k & M2) * SW + c] = emis_df(xraw[(k & MX) * g.xstride + c], lser[k & MX].x);
+      emis[(k & M2) * SW + c] = emis_log2(xraw[(k & MX) * g.xstride + c], lser[k & MX].x);
     }
   };
   // Gradient rows of a finished phase-2 epoch, lane = row (ctc.cpp:196-203,
@@ -597,6 +559,13 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   // Chain warps: the recursion, and one step behind it (same basic block,
   // so the scheduler fills the recursion's latency gaps with it) the
   // column's storage (phase 1) or occupancies (phase 2).
+  //
+  // Carried representation ("offset log"): a cell's value in log2 units is
+  // O + r, with ONE integer-valued fp32 offset O per chain thread and fp32
+  // residuals r per cell. Every step re-centres O on the thread's largest
+  // cell, so the cells that carry the mass have |r| < 1 (fp32 resolution
+  // 2^-24) however large |alpha| grows over T frames; offsets of different
+  // threads differ by integers, so aligning a neighbour's value is exact.
   // =====================================================================
   // Emission-row index of each cell; cells that do not exist read the
   // sentinel column (no predicate between the loads and their use).
@@ -611,17 +580,18 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     sidx_b[p] = has_b[p] ? (fused ? a.blank : 0) : g.SW;
     skip[p] = is_chain && i >= 1 && i < L && s_lab[i] != a.blank && s_lab[i] != s_lab[i - 1];
   }
-  DF vb[K], vl[K];  // carried values: alpha (forward) or emission-inclusive beta~ (backward)
-  DF xb[K], xl[K];  // backward only: emission-exclusive beta (what storage / occupancy use)
-  float2 eB[K], eL[K];
+  float vb[K], vl[K];  // carried residuals: alpha (forward) or emission-inclusive beta~ (backward)
+  float xb[K], xl[K];  // backward only: emission-exclusive beta (what storage / occupancy use)
+  float O = 0.f;       // this thread's offset (integer valued)
+  float eB[K], eL[K];
 #pragma unroll
   for (int p = 0; p < K; ++p) {
-    vb[p] = vl[p] = xb[p] = xl[p] = sent();
-    eB[p] = eL[p] = make_float2(SENT, 0.f);
+    vb[p] = vl[p] = xb[p] = xl[p] = SENT;
+    eB[p] = eL[p] = SENT;
   }
 
   auto load_emis = [&](int k) {
-    const float2* er = emis + (k & M2) * SW;
+    const float* er = emis + (k & M2) * SW;
 #pragma unroll
     for (int p = 0; p < K; ++p) {
       eB[p] = er[sidx_b[p]];
@@ -633,104 +603,105 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     for (int p = 0; p < K; ++p) {
       const int i = ctid * K + p;
       if (dir == 0) {  // alpha(s, 0) = lp(0, aug[s]) for s < 2 (ctc.cpp:114)
-        vb[p] = i == 0 ? DF{eB[p].x, eB[p].y} : sent();
-        vl[p] = i == 0 ? DF{eL[p].x, eL[p].y} : sent();
+        vb[p] = i == 0 ? eB[p] : SENT;
+        vl[p] = i == 0 ? eL[p] : SENT;
       } else {  // beta(s, T-1) = 0 for s >= S-2 (ctc.cpp:130)
         const bool last = i == L;
-        xb[p] = last ? DF{0.f, 0.f} : sent();
-        xl[p] = last ? DF{0.f, 0.f} : sent();
-        vb[p] = last ? incl(DF{0.f, 0.f}, 0.f, eB[p]) : sent();
-        vl[p] = last ? incl(DF{0.f, 0.f}, 0.f, eL[p]) : sent();
+        xb[p] = last ? 0.f : SENT;
+        xl[p] = last ? 0.f : SENT;
+        vb[p] = last ? eB[p] : SENT;
+        vl[p] = last ? eL[p] : SENT;
       }
     }
-    if (dir == 0) st_tagged(lane == 31 && cwarp + 1 < nw_u, bnd + cwarp * P2, vl[K - 1], 0);
-    else st_tagged(lane == 0 && cwarp > 0, bnd + cwarp * P2, vl[0], 0);
+    if (dir == 0) st_tagged(lane == 31 && cwarp + 1 < nw_u, bnd + cwarp * P2, vl[K - 1], O, 0);
+    else st_tagged(lane == 0 && cwarp > 0, bnd + cwarp * P2, vl[0], O, 0);
   };
-  // Neighbour value for step k: a shuffle inside the warp; across warps the
-  // tagged boundary slot, prefetched one step early (the upstream warp runs
-  // ahead: its boundary cell depends on the far side of the warp only K
-  // steps later), re-polled if stale.
+  // Neighbour cell for step k as (residual, offset): a shuffle inside the
+  // warp; across warps the tagged boundary slot, prefetched one step early
+  // (the upstream warp runs ahead: its boundary cell depends on the far side
+  // of the warp only K steps later), re-polled if stale.
   unsigned long long bpre = ~0ull;
   const int up_w = dir == 0 ? cwarp - 1 : cwarp + 1;  // upstream warp
   // vote results are warp-uniform, so branches on them need no reconvergence
   const bool has_up = __all_sync(0xffffffffu, up_w >= 0 && up_w < nw_u);
   const bool edge_lane = lane == (dir == 0 ? 0 : 31);
-  auto neighbour = [&](int k) -> DF {
-    DF nb;
+  struct Nb {
+    float r, o;
+  };
+  auto neighbour = [&](int k) -> Nb {
+    Nb nb;
     if (dir == 0) {
-      nb.h = __shfl_up_sync(0xffffffffu, vl[K - 1].h, 1);
-      nb.l = __shfl_up_sync(0xffffffffu, vl[K - 1].l, 1);
+      nb.r = __shfl_up_sync(0xffffffffu, vl[K - 1], 1);
+      nb.o = __shfl_up_sync(0xffffffffu, O, 1);
     } else {
-      nb.h = __shfl_down_sync(0xffffffffu, vl[0].h, 1);
-      nb.l = __shfl_down_sync(0xffffffffu, vl[0].l, 1);
+      nb.r = __shfl_down_sync(0xffffffffu, vl[0], 1);
+      nb.o = __shfl_down_sync(0xffffffffu, O, 1);
     }
 #ifdef DS2CTC_EXP_NOBND
-    if (edge_lane) nb = sent();
+    if (edge_lane) nb = {SENT, O};
     return nb;
 #endif
     unsigned long long v = bpre;
     const bool stale = (v & 0xFFull) != (static_cast<unsigned long long>(k - 1) & 0xFFull);
-    if (has_up && __any_sync(0xffffffffu, stale)) {
-      const DF w = ld_tagged(bnd + up_w * P2 + ((k - 1) & M2), k - 1);
-      v = tag_pack(w, k - 1);
-    }
-    const DF bv = tag_unpack(v);
-    if (edge_lane) nb = has_up ? bv : sent();
+    if (has_up && __any_sync(0xffffffffu, stale)) v = ld_tagged(bnd + up_w * P2 + ((k - 1) & M2), k - 1);
+    if (edge_lane) nb = has_up ? Nb{tag_r(v), tag_o(v)} : Nb{SENT, O};
     return nb;
   };
-  auto step = [&](int k, DF nb) {  // column k from column k - 1, k >= 1
-    DF nvb[K], nvl[K];
+  auto step = [&](int k, Nb nb) {  // column k from column k - 1, k >= 1
+    const float n0 = nb.r + (nb.o - O);  // the neighbour in this thread's offset (exact offset difference)
+    float nvb[K], nvl[K];
 #pragma unroll
     for (int q = 0; q < K; ++q) {
       const int p = dir == 0 ? q : K - 1 - q;
-      const DF n1 = dir == 0 ? (p == 0 ? nb : vl[p - 1]) : (p == K - 1 ? nb : vl[p + 1]);
-      DF mb, ml;
-      const float cb = lse2(vb[p], n1, mb);                            // blank 2i <- 2i, 2i -+ 1
-      const float cl = lse3(vl[p], vb[p], skip[p] ? n1 : sent(), ml);  // label <- itself, blank 2i, 2i -+ 1
-      nvb[p] = incl(mb, cb, eB[p]);
-      nvl[p] = incl(ml, cl, eL[p]);
+      const float n1 = dir == 0 ? (p == 0 ? n0 : vl[p - 1]) : (p == K - 1 ? n0 : vl[p + 1]);
+      const float mb = lse2f(vb[p], n1);                            // blank 2i <- 2i, 2i -+ 1
+      const float ml = lse3f(vl[p], vb[p], skip[p] ? n1 : SENT);  // label <- itself, blank 2i, 2i -+ 1
+      nvb[p] = mb + eB[p];
+      nvl[p] = ml + eL[p];
       if (dir == 1) {
-        xb[p] = excl(mb, cb);
-        xl[p] = excl(ml, cl);
+        xb[p] = mb;
+        xl[p] = ml;
       }
     }
+    // re-centre on the largest cell (dead threads adopt the upstream offset,
+    // so the first mass to arrive is aligned exactly)
+    float mx = fmaxf(nvb[0], nvl[0]);
+#pragma unroll
+    for (int p = 1; p < K; ++p) mx = fmaxf(mx, fmaxf(nvb[p], nvl[p]));
+    const bool live = mx > SENT_CUT;
+    const float sh = live ? rintf(mx) : 0.f;
 #pragma unroll
     for (int p = 0; p < K; ++p) {
-      vb[p] = nvb[p];
-      vl[p] = nvl[p];
+      vb[p] = nvb[p] - sh;
+      vl[p] = nvl[p] - sh;
+      if (dir == 1) {
+        xb[p] -= sh;
+        xl[p] -= sh;
+      }
     }
+    O = live ? O + sh : nb.o;
     const int down = dir == 0 ? cwarp + 1 : cwarp - 1;
-    if (dir == 0) st_tagged(lane == 31 && down < nw_u, bnd + cwarp * P2 + (k & M2), vl[K - 1], k);
-    else st_tagged(lane == 0 && down >= 0, bnd + cwarp * P2 + (k & M2), vl[0], k);
+    if (dir == 0) st_tagged(lane == 31 && down < nw_u, bnd + cwarp * P2 + (k & M2), vl[K - 1], O, k);
+    else st_tagged(lane == 0 && down >= 0, bnd + cwarp * P2 + (k & M2), vl[0], O, k);
     asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(bpre) : "r"(smem_addr(bnd + max(up_w, 0) * P2 + (k & M2))));
   };
 
-  // Phase 1: column k -> fp32 deltas from this thread's own max hi part (no
-  // cross-lane reduction). Sentinel cells need no special case: their deltas
-  // (or the offset itself) stay below -1e29 and give 2^gamma = 0.
+  // Phase 1: column k -> the stored half-lattice: the residuals in slot
+  // order and the thread's offset (value = offset + residual).
   const bool stores = is_chain && ctid < column_threads(L, K);
   auto store_column = [&](int k, const Epoch& e) {
 #ifdef DS2CTC_EXP_NOSTORE
     return;
 #endif
-    DF cb[K], clv[K];  // static selects: a pointer to either register array would live in local memory
-#pragma unroll
-    for (int p = 0; p < K; ++p) {
-      cb[p] = dir == 0 ? vb[p] : xb[p];
-      clv[p] = dir == 0 ? vl[p] : xl[p];
-    }
-    float hm = fmaxf(cb[0].h, clv[0].h);
-#pragma unroll
-    for (int p = 1; p < K; ++p) hm = fmaxf(hm, fmaxf(cb[p].h, clv[p].h));
     float* dst = cb_row(k, e) + 2 * K * ctid;
     float v[2 * K];
 #pragma unroll
     for (int p = 0; p < K; ++p) {
-      const float db = (cb[p].h - hm) + cb[p].l;
-      const float dl = (clv[p].h - hm) + clv[p].l;
+      const float cbv = dir == 0 ? vb[p] : xb[p];
+      const float clv = dir == 0 ? vl[p] : xl[p];
       // forward pair = slots (blank 2i, label 2i+1); backward = (label 2i-1, blank 2i) at +1
-      v[2 * p] = dir == 0 ? db : dl;
-      v[2 * p + 1] = dir == 0 ? dl : db;
+      v[2 * p] = dir == 0 ? cbv : clv;
+      v[2 * p + 1] = dir == 0 ? clv : cbv;
     }
     if (stores) {
       if (K % 2 == 0) {
@@ -741,7 +712,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
 #pragma unroll
         for (int p = 0; p < K; ++p) reinterpret_cast<float2*>(dst)[p] = make_float2(v[2 * p], v[2 * p + 1]);
       }
-      (dst - 2 * K * ctid)[OB + ctid] = hm;
+      (dst - 2 * K * ctid)[OB + ctid] = O;
     }
   };
 
@@ -762,24 +733,24 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     float d[2 * K];
 #pragma unroll
     for (int q = 0; q < 2 * K; ++q) d[q] = row[max(pslot0 + q, 0)];
-    const float off_lo = row[poff_lo], off_hi = row[poff_hi];
+    // gamma = alpha + beta - log Z (plain add, ctc.cpp:200); the carried
+    // offset was shifted by -log Z at the meet, so the offsets add exactly
+    // and only the residuals round.
+    const float o_lo = row[poff_lo] + O, o_hi = row[poff_hi] + O;
     float* ebr = eb + (k & M2) * g.estride;
     float* elr = el + (k & M2) * g.estride;
 #pragma unroll
     for (int p = 0; p < K; ++p) {
       const int i = ctid * K + p;
-      const DF vbp = dir == 0 ? vb[p] : xb[p];
-      const DF vlp = dir == 0 ? vl[p] : xl[p];
+      const float rb = dir == 0 ? vb[p] : xb[p];
+      const float rl = dir == 0 ? vl[p] : xl[p];
       // cell positions among the lane's 2K partner slots, and their writer thread
       const int qb = dir == 0 ? 2 * p : 2 * p + 1;
       const int ql = dir == 0 ? 2 * p + 1 : 2 * p;
-      const float ob = (dir == 0 ? qb == 2 * K - 1 : qb != 0) ? off_hi : off_lo;
-      const float ol = (dir == 0 ? ql == 2 * K - 1 : ql != 0) ? off_hi : off_lo;
-      // gamma = alpha + beta - log Z (plain add, ctc.cpp:200); the carried
-      // values were shifted by -log Z at the meet, so this is one
-      // near-cancelling add of the partner's offset plus the small parts.
-      const float o_b = ex2((vbp.h + ob) + (vbp.l + d[qb]));
-      const float o_l = ex2((vlp.h + ol) + (vlp.l + d[ql]));
+      const float ob = (dir == 0 ? qb == 2 * K - 1 : qb != 0) ? o_hi : o_lo;
+      const float ol = (dir == 0 ? ql == 2 * K - 1 : ql != 0) ? o_hi : o_lo;
+      const float o_b = ex2(ob + (rb + d[qb]));
+      const float o_l = ex2(ol + (rl + d[ql]));
       if (has_b[p]) ebr[i] = o_b;
       if (has_l[p]) elr[dir == 0 ? i : i - 1] = o_l;
     }
@@ -803,7 +774,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     if (ph2) {
       for (int k = e.k0 + 1; k < e.k1; ++k) {
         STEP_STAMP(k, e, 0);
-        const DF nb = neighbour(k);
+        const Nb nb = neighbour(k);
         occupancy_column(k - 1, e);
         step(k, nb);
         load_emis(k + 1);
@@ -813,7 +784,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     } else {
       for (int k = e.k0 + 1; k < e.k1; ++k) {
         STEP_STAMP(k, e, 0);
-        const DF nb = neighbour(k);
+        const Nb nb = neighbour(k);
         store_column(k - 1, e);
         step(k, nb);
         load_emis(k + 1);
@@ -930,29 +901,24 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
         for (int w = 0; w < NT / 32; ++w) tot += red[32 + w];
         logz2 = M + log2(tot);
       }
-      Zh = static_cast<float>(logz2);
-      Zl = static_cast<float>(logz2 - static_cast<double>(Zh));
       dead = logz2 == -__builtin_huge_val();  // zero-probability lattice (ctc.cpp:189-193)
       if (dead || !want_grad) break;
       if (is_chain) {
-        // Shift the carried column by -log Z (the recursion is shift-invariant),
-        // so phase-2 occupancies need no large subtraction, and re-publish
-        // the boundary cell of step kmid with the shift applied.
-        auto shift = [&](DF v) -> DF {
-          const DF t = two_sum(v.h, -Zh);
-          const float lo = t.l + (v.l - Zl);
-          const float h = t.h + lo;
-          return {h, lo - (h - t.h)};
-        };
+        // Shift the carried column by -log Z (the recursion is shift-invariant):
+        // the integer part goes into the offset (exact), the fraction into
+        // the residuals; then re-publish the boundary cell of step kmid.
+        const double zi = rint(logz2);
+        const float zf = static_cast<float>(logz2 - zi);
+        O -= static_cast<float>(zi);
 #pragma unroll
         for (int p = 0; p < K; ++p) {
-          vb[p] = shift(vb[p]);
-          vl[p] = shift(vl[p]);
-          xb[p] = shift(xb[p]);
-          xl[p] = shift(xl[p]);
+          vb[p] -= zf;
+          vl[p] -= zf;
+          xb[p] -= zf;
+          xl[p] -= zf;
         }
-        if (dir == 0) st_tagged(lane == 31 && cwarp + 1 < nw_u, bnd + cwarp * P2 + (kmid & M2), vl[K - 1], kmid);
-        else st_tagged(lane == 0 && cwarp > 0, bnd + cwarp * P2 + (kmid & M2), vl[0], kmid);
+        if (dir == 0) st_tagged(lane == 31 && cwarp + 1 < nw_u, bnd + cwarp * P2 + (kmid & M2), vl[K - 1], O, kmid);
+        else st_tagged(lane == 0 && cwarp > 0, bnd + cwarp * P2 + (kmid & M2), vl[0], O, kmid);
         bpre = ~0ull;
       }
       if (service && lane == 0) {
