@@ -232,6 +232,11 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned parity
 __device__ long long g_epoch_clock[2][128][33][2];
 // per-step stamps of epoch 1 for warps 0..7 (lane 0): [cta][warp][step][point]
 __device__ long long g_step_clock[2][8][32][4];
+__device__ long long g_meet_clock[2][8];
+#define MEET_STAMP(i) \
+  do {                \
+    if (blockIdx.x < 2 && tid == 0) g_meet_clock[dir][i] = clock64(); \
+  } while (0)
 #define STEP_STAMP(k, e, pt)                                                                            \
   do {                                                                                                  \
     if (blockIdx.x < 2 && lane == 0 && warp < 7 && (e).phase == 2 && (e).k0 == k2s + 2 * P &&           \
@@ -241,6 +246,9 @@ __device__ long long g_step_clock[2][8][32][4];
 #else
 #define STEP_STAMP(k, e, pt) \
   do {                       \
+  } while (0)
+#define MEET_STAMP(i) \
+  do {                \
   } while (0)
 #endif
 
@@ -305,7 +313,6 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   float* xraw = reinterpret_cast<float*>(smem + g.off_xraw);
   float* emis = reinterpret_cast<float*>(smem + g.off_emis);
   float2* lser = reinterpret_cast<float2*>(smem + g.off_lse);
-  float* eb = reinterpret_cast<float*>(smem + g.off_eb);
   float* el = reinterpret_cast<float*>(smem + g.off_el);
   float* tile = reinterpret_cast<float*>(smem + g.off_tile);
   float* occs = reinterpret_cast<float*>(smem + g.off_occ);
@@ -478,48 +485,41 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     if (e.phase != 2) return;
     const int n = e.k1 - e.k0;
     const int k = e.k0 + (lane < n ? lane : 0);
-    const float* ebr = eb + (k & M2) * g.estride;
     const float* elr = el + (k & M2) * g.estride;
     float* oc = occs + lane * g.ostride;
-    // blank rows (every even lattice row), four independent partial sums
-    float b0 = 0.f, b1 = 0.f, b2 = 0.f, b3 = 0.f;
-    int i = 0;
-    for (; i + 3 <= L; i += 4) {
-      b0 += ebr[i];
-      b1 += ebr[i + 1];
-      b2 += ebr[i + 2];
-      b3 += ebr[i + 3];
-    }
-    for (; i <= L; ++i) b0 += ebr[i];
-    // label rows in one flat pass over the slot-sorted positions (slot 0 =
-    // label positions carrying the blank id), flushing at slot changes
-    float acc = 0.f;
-    int cur = 0;
-    int q = 0;
+    // Label cells in one flat pass over the slot-sorted positions of slots
+    // >= 1 (every one of them has positions), flushing at slot changes. The
+    // blank slot is the rest of the frame's unit mass: sum_s gamma(s, t) = 1
+    // for every t (each path visits one lattice row per frame), so
+    // occ(blank) = (blank rows + label positions carrying the blank id)
+    //            = 1 - sum of the other slots.
+    float acc = 0.f, tot = 0.f;
+    int cur = 1;
+    int q = s_kstart[1];
     for (; q + 3 < L; q += 4) {
       const int w0 = s_kq[q], w1 = s_kq[q + 1], w2 = s_kq[q + 2], w3 = s_kq[q + 3];
       const float v0 = elr[w0 & 0xFFFF], v1 = elr[w1 & 0xFFFF], v2 = elr[w2 & 0xFFFF], v3 = elr[w3 & 0xFFFF];
       const int j0 = w0 >> 16, j1 = w1 >> 16, j2 = w2 >> 16, j3 = w3 >> 16;
-      if (j0 != cur) { oc[cur] = acc; acc = 0.f; cur = j0; }
+      if (j0 != cur) { oc[cur] = acc; tot += acc; acc = 0.f; cur = j0; }
       acc += v0;
-      if (j1 != cur) { oc[cur] = acc; acc = 0.f; cur = j1; }
+      if (j1 != cur) { oc[cur] = acc; tot += acc; acc = 0.f; cur = j1; }
       acc += v1;
-      if (j2 != cur) { oc[cur] = acc; acc = 0.f; cur = j2; }
+      if (j2 != cur) { oc[cur] = acc; tot += acc; acc = 0.f; cur = j2; }
       acc += v2;
-      if (j3 != cur) { oc[cur] = acc; acc = 0.f; cur = j3; }
+      if (j3 != cur) { oc[cur] = acc; tot += acc; acc = 0.f; cur = j3; }
       acc += v3;
     }
     for (; q < L; ++q) {
       const int w0 = s_kq[q];
       const int j0 = w0 >> 16;
-      if (j0 != cur) { oc[cur] = acc; acc = 0.f; cur = j0; }
+      if (j0 != cur) { oc[cur] = acc; tot += acc; acc = 0.f; cur = j0; }
       acc += elr[w0 & 0xFFFF];
     }
-    oc[cur] = acc;
-    // slots without positions (the blank slot when no label uses the blank id)
-    for (int j = 0; j < u.nkey; ++j)
-      if (s_kstart[j] == s_kstart[j + 1]) oc[j] = 0.f;
-    oc[0] += (b0 + b1) + (b2 + b3);
+    if (u.nkey > 1) {
+      oc[cur] = acc;
+      tot += acc;
+    }
+    oc[0] = 1.f - tot;
     float* tr = tile + lane * g.tstride;
     if (fused) {
       const float2 st = lser[k & MX];
@@ -656,12 +656,10 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
       const float n1 = dir == 0 ? (p == 0 ? n0 : vl[p - 1]) : (p == K - 1 ? n0 : vl[p + 1]);
       const float mb = lse2f(vb[p], n1);                            // blank 2i <- 2i, 2i -+ 1
       const float ml = lse3f(vl[p], vb[p], skip[p] ? n1 : SENT);  // label <- itself, blank 2i, 2i -+ 1
-      nvb[p] = mb + eB[p];
-      nvl[p] = ml + eL[p];
-      if (dir == 1) {
-        xb[p] = mb;
-        xl[p] = ml;
-      }
+      // forward: alpha = lse + emission; backward: the lse IS the
+      // emission-exclusive beta, the carried value adds the emission
+      nvb[p] = dir == 0 ? mb + eB[p] : mb;
+      nvl[p] = dir == 0 ? ml + eL[p] : ml;
     }
     // re-centre on the largest cell (dead threads adopt the upstream offset,
     // so the first mass to arrive is aligned exactly)
@@ -672,11 +670,14 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     const float sh = live ? rintf(mx) : 0.f;
 #pragma unroll
     for (int p = 0; p < K; ++p) {
-      vb[p] = nvb[p] - sh;
-      vl[p] = nvl[p] - sh;
-      if (dir == 1) {
-        xb[p] -= sh;
-        xl[p] -= sh;
+      if (dir == 0) {
+        vb[p] = nvb[p] - sh;
+        vl[p] = nvl[p] - sh;
+      } else {
+        xb[p] = nvb[p] - sh;
+        xl[p] = nvl[p] - sh;
+        vb[p] = xb[p] + eB[p];
+        vl[p] = xl[p] + eL[p];
       }
     }
     O = live ? O + sh : nb.o;
@@ -716,13 +717,16 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     }
   };
 
-  // Phase 2: occupancies from the partner's stored columns, which the
-  // service warp bulk-loads (TMA) into the column buffer one epoch ahead.
-  // The partner's slot of cell s is s + 1 when the partner is the backward
-  // CTA and s when it is the forward one: a forward lane's cells sit at
-  // partner slots 2*ctid*K + 1 .. 2*ctid*K + 2K, a backward lane's at
-  // 2*ctid*K - 1 .. 2*ctid*K + 2K - 2 (slot -1 belongs to no cell).
-  const int pslot0 = 2 * K * ctid + (dir == 0 ? 1 : -1);
+  // Phase 2: label-cell occupancies from the partner's stored columns,
+  // which the service warp bulk-loads (TMA) into the column buffer one epoch
+  // ahead (blank cells are not needed: the gradient warp takes the blank
+  // slot as the rest of the frame's unit mass). The partner stores cell s at
+  // slot s + 1 (backward partner) or s (forward partner): this lane's label
+  // cells 2i+1 (forward) sit at partner slots 2i+2, label cells 2i-1
+  // (backward) at 2i-1; the last forward label belongs to the next thread.
+  int pslot[K];
+#pragma unroll
+  for (int p = 0; p < K; ++p) pslot[p] = max(2 * K * ctid + 2 * p + (dir == 0 ? 2 : -1), 0);
   const int poff_lo = OB + max(dir == 0 ? ctid : ctid - 1, 0);  // writer threads of the first / last slot
   const int poff_hi = OB + (dir == 0 ? ctid + 1 : ctid);
   auto occupancy_column = [&](int k, const Epoch& e) {
@@ -730,28 +734,17 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     return;
 #endif
     const float* row = cb_row(k, e);
-    float d[2 * K];
-#pragma unroll
-    for (int q = 0; q < 2 * K; ++q) d[q] = row[max(pslot0 + q, 0)];
     // gamma = alpha + beta - log Z (plain add, ctc.cpp:200); the carried
     // offset was shifted by -log Z at the meet, so the offsets add exactly
     // and only the residuals round.
     const float o_lo = row[poff_lo] + O, o_hi = row[poff_hi] + O;
-    float* ebr = eb + (k & M2) * g.estride;
     float* elr = el + (k & M2) * g.estride;
 #pragma unroll
     for (int p = 0; p < K; ++p) {
       const int i = ctid * K + p;
-      const float rb = dir == 0 ? vb[p] : xb[p];
       const float rl = dir == 0 ? vl[p] : xl[p];
-      // cell positions among the lane's 2K partner slots, and their writer thread
-      const int qb = dir == 0 ? 2 * p : 2 * p + 1;
-      const int ql = dir == 0 ? 2 * p + 1 : 2 * p;
-      const float ob = (dir == 0 ? qb == 2 * K - 1 : qb != 0) ? o_hi : o_lo;
-      const float ol = (dir == 0 ? ql == 2 * K - 1 : ql != 0) ? o_hi : o_lo;
-      const float o_b = ex2(ob + (rb + d[qb]));
-      const float o_l = ex2(ol + (rl + d[ql]));
-      if (has_b[p]) ebr[i] = o_b;
+      const float ol = (dir == 0 ? p == K - 1 : p != 0) ? o_hi : o_lo;
+      const float o_l = ex2(ol + (rl + row[pslot[p]]));
       if (has_l[p]) elr[dir == 0 ? i : i - 1] = o_l;
     }
   };
@@ -846,7 +839,9 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
       // the previous epoch's half must be read out before the next epoch refills it
       if (lane == 0 && cur.phase == 1) bulk_wait_read0();
     } else if (grad_warp) {
+#ifndef DS2CTC_EXP_NOGRAD
       grad_rows(prev);
+#endif
     } else if (is_chain) {
       chain_epoch(cur);
     }
@@ -857,11 +852,14 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     __syncthreads();
     if (cur.phase == 1 && cur.k1 == kmid + 1) {
       // ---- meet in the middle: log Z (all threads of both CTAs) ----
+      MEET_STAMP(0);
       if (service && lane == 0) {
         store_epoch(cur, ep & 1);
         bulk_wait0();  // every stored column is in global memory before the partner reads it
       }
+      MEET_STAMP(1);
       cluster_barrier();
+      MEET_STAMP(2);
       // Both CTAs read the two STORED columns (alpha(tm) at column T, beta(tm)
       // at column tm) with the same cell->thread map and reduction order, so
       // they derive the bitwise-identical log Z.
@@ -902,6 +900,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
         logz2 = M + log2(tot);
       }
       dead = logz2 == -__builtin_huge_val();  // zero-probability lattice (ctc.cpp:189-193)
+      MEET_STAMP(3);
       if (dead || !want_grad) break;
       if (is_chain) {
         // Shift the carried column by -log Z (the recursion is shift-invariant):
@@ -925,7 +924,9 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
         fence_async_all();  // the partner's bulk stores (ordered by the cluster barrier) -> our bulk loads
         load_epoch(nxt, (ep + 1) & 1);
       }
+      MEET_STAMP(4);
       __syncthreads();
+      MEET_STAMP(5);
     }
     prev = cur;
     cur = nxt;
@@ -982,6 +983,9 @@ int launch_k(const PairArgs& a, void* stream) {
 #ifdef DS2CTC_EPOCH_TIMING
 extern "C" int ds2ctc_debug_epoch_clocks(long long* host) {
   return cudaMemcpyFromSymbol(host, g_epoch_clock, sizeof(g_epoch_clock));
+}
+extern "C" int ds2ctc_debug_meet_clocks(long long* host) {
+  return cudaMemcpyFromSymbol(host, g_meet_clock, sizeof(g_meet_clock));
 }
 extern "C" int ds2ctc_debug_step_clocks(long long* host) {
   return cudaMemcpyFromSymbol(host, g_step_clock, sizeof(g_step_clock));

@@ -58,7 +58,7 @@ struct Geometry {
   int max_L;
   int fused;
   // shared-memory carve-up (bytes, 16-aligned)
-  int off_xraw, off_emis, off_lse, off_eb, off_el, off_tile, off_occ, off_bnd, off_meta, off_red;
+  int off_xraw, off_emis, off_lse, off_el, off_tile, off_occ, off_bnd, off_meta, off_red;
   int off_cb;     // column buffer [2][P][cw_max] floats (TMA bulk stores / loads of lattice columns)
   int off_mbar;   // two mbarriers (one per column-buffer half)
   int xstride;    // floats per xraw row (odd)
@@ -115,9 +115,8 @@ inline Geometry make_geometry(int max_L_all, int max_L, int max_nkey, int A, boo
     };
     const int RX = 4 * P;
     g.off_xraw = take(4 * RX * g.xstride);
-    g.off_emis = take(8 * 2 * P * (g.SW + 1));  // + a sentinel column for cells that do not exist
+    g.off_emis = take(4 * 2 * P * (g.SW + 1));  // + a sentinel column for cells that do not exist
     g.off_lse = take(8 * RX);
-    g.off_eb = take(4 * 2 * P * g.estride);
     g.off_el = take(4 * 2 * P * g.estride);
     g.off_tile = take(4 * 32 * g.tstride);  // one row per service lane (all 32 lanes run, P <= 32)
     g.off_occ = take(4 * 32 * g.ostride);

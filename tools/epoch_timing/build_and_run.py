@@ -69,6 +69,12 @@ def run(so, A=29, T=700, L=150, B=64, brief=False):
             print(f"  k+{k:2d} " + "  ".join(row))
     print("TIGHT cycles/step: critical", steps[0, 7, 31, 3] / 1000.0, "| + load_emis", steps[0, 7, 31, 2] / 1000.0,
           "| + stamps & real k", steps[0, 7, 31, 1] / 1000.0)
+    meet = np.zeros((2, 8), dtype=np.int64)
+    if lib.ds2ctc_debug_meet_clocks(meet.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong))) == 0:
+        for cta in range(2):
+            m = meet[cta]
+            print(f"  cta{cta}: meet: store+wait {m[1]-m[0]}, cluster barrier {m[2]-m[1]}, logZ {m[3]-m[2]}, "
+                  f"shift+load {m[4]-m[3]}, sync {m[5]-m[4]}")
     if brief:
         for cta in range(2):
             rows = [buf[cta, e] for e in range(128) if buf[cta, e, 0, 0] != 0]
