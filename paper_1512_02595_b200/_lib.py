@@ -11,7 +11,8 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libds2ctc.so")
+# DS2CTC_LIB: debug experiments only (a variant build of the same sources, see build.build_variant)
+LIB_PATH = os.environ.get("DS2CTC_LIB") or os.path.join(PKG, "libds2ctc.so")
 
 STATUS = {
     0: "SUCCESS",

@@ -39,37 +39,50 @@ def _newer(target: str, deps) -> bool:
     return all(os.path.getmtime(d) <= t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB, build_dir: str = BUILD) -> str:
+    """Builds the library. `defines` (debug experiments only, e.g. ("DS2CTC_EXP_NOOCC",))
+    go to a separate `lib` / `build_dir`; the product library is built without any."""
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(INCLUDE, "ds2ctc.h"), __file__]
-    if not force and _newer(LIB, deps):
-        return LIB
-    os.makedirs(BUILD, exist_ok=True)
+    if not force and _newer(lib, deps):
+        return lib
+    LIB_ = lib
+    BUILD_ = build_dir
+    os.makedirs(BUILD_, exist_ok=True)
     cc = nvcc()
-    common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC,-Wall", f"-I{INCLUDE}", f"-I{CSRC}"]
+    common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC,-Wall", f"-I{INCLUDE}", f"-I{CSRC}",
+              *[f"-D{d}" for d in defines]]
     objs = []
     for src in CU_SOURCES:
-        obj = os.path.join(BUILD, src + ".o")
+        obj = os.path.join(BUILD_, src + ".o")
         cmd = [cc, *ARCH, "-lineinfo", "-Xptxas", "-v", *common, "-c", os.path.join(CSRC, src), "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed:\n{' '.join(cmd)}\n{res.stderr}")
-        with open(os.path.join(BUILD, src + ".ptxas.txt"), "w") as f:
+        with open(os.path.join(BUILD_, src + ".ptxas.txt"), "w") as f:
             f.write(res.stderr)
         if verbose:
             print(res.stderr)
         objs.append(obj)
     cuda_inc = os.path.join(os.path.dirname(os.path.dirname(cc)), "include")
     for src in CPP_SOURCES:
-        obj = os.path.join(BUILD, src + ".o")
+        obj = os.path.join(BUILD_, src + ".o")
         cmd = [os.environ.get("CXX", "g++"), "-O3", "-std=c++17", "-fPIC", "-Wall", "-Wextra", f"-I{INCLUDE}",
                f"-I{CSRC}", f"-I{cuda_inc}", "-c", os.path.join(CSRC, src), "-o", obj]
         subprocess.run(cmd, check=True)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = LIB_ + ".tmp"
     subprocess.run([cc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-lpthread", "-ldl", "-lrt"],
                    check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, LIB_)
+    return LIB_
+
+
+def build_variant(name: str, defines) -> str:
+    """Debug-experiment library build/variants/libds2ctc_<name>.so (bench.py picks
+    it up through DS2CTC_LIB); never used by the product path."""
+    out = os.path.join(ROOT, "build", "variants")
+    return build(force=True, defines=defines, lib=os.path.join(out, f"libds2ctc_{name}.so"),
+                 build_dir=os.path.join(out, name))
 
 
 if __name__ == "__main__":

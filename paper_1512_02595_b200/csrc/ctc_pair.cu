@@ -137,6 +137,25 @@ __device__ __forceinline__ void bulk_load(float* sdst, const float* gsrc, int by
       : "memory");
 }
 
+// Predicated shared stores (no branch around them in the recursion loop).
+__device__ __forceinline__ void sts4_if(bool pred, float* p, float a, float b, float c, float d) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t@q st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n\t}" ::"r"(
+                   smem_addr(p)),
+               "f"(a), "f"(b), "f"(c), "f"(d), "r"(static_cast<unsigned>(pred))
+               : "memory");
+}
+__device__ __forceinline__ void sts2_if(bool pred, float* p, float a, float b) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q st.shared.v2.f32 [%0], {%1, %2};\n\t}" ::"r"(
+                   smem_addr(p)),
+               "f"(a), "f"(b), "r"(static_cast<unsigned>(pred))
+               : "memory");
+}
+__device__ __forceinline__ void sts1_if(bool pred, float* p, float a) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.f32 [%0], %1;\n\t}" ::"r"(smem_addr(p)),
+               "f"(a), "r"(static_cast<unsigned>(pred))
+               : "memory");
+}
+
 // Predicated global stores (no branch around them in the recursion loop).
 __device__ __forceinline__ void st_global2_if(bool pred, float* p, float x, float y) {
   asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t@p st.global.v2.f32 [%0], {%1, %2};\n\t}" ::"l"(p),
@@ -233,6 +252,7 @@ __device__ long long g_epoch_clock[2][128][33][2];
 // per-step stamps of epoch 1 for warps 0..7 (lane 0): [cta][warp][step][point]
 __device__ long long g_step_clock[2][8][32][4];
 __device__ long long g_meet_clock[2][8];
+__device__ long long g_kernel_end[2];
 #define MEET_STAMP(i) \
   do {                \
     if (blockIdx.x < 2 && tid == 0) g_meet_clock[dir][i] = clock64(); \
@@ -325,6 +345,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   int* s_kq = s_slotpos + L + 1;  // slot-sorted positions packed as pos | slot << 16
   short* s_slot = reinterpret_cast<short*>(s_kq + L + 1);  // fused: symbol -> slot
   double* red = reinterpret_cast<double*>(smem + g.off_red);
+  float* sdummy = reinterpret_cast<float*>(smem + g.off_dummy);  // write sink of threads without cells
   // Column buffer [2][P][cw]: phase 1 = this CTA's columns of an epoch (bulk
   // stored by the service warp after the epoch), phase 2 = the partner's
   // columns of an epoch (bulk loaded one epoch ahead). Row r of an epoch is
@@ -338,6 +359,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   };
 
   // ---- prologue: per-utterance metadata into shared memory ----
+  MEET_STAMP(6);
   for (int i = tid; i < L; i += NT) s_lab[i] = a.labels[u.lab_off + i];
   for (int j = tid; j < u.nkey; j += NT) s_kchar[j] = a.key_char[u.key_off + j];
   for (int j = tid; j <= u.nkey; j += NT) s_kstart[j] = a.key_start[u.key_off + b + j];
@@ -644,7 +666,11 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     unsigned long long v = bpre;
     const bool stale = (v & 0xFFull) != (static_cast<unsigned long long>(k - 1) & 0xFFull);
     if (has_up && __any_sync(0xffffffffu, stale)) v = ld_tagged(bnd + up_w * P2 + ((k - 1) & M2), k - 1);
-    if (edge_lane) nb = has_up ? Nb{tag_r(v), tag_o(v)} : Nb{SENT, O};
+    // selects, not a branch on the edge lane
+    const float er = has_up ? tag_r(v) : SENT;
+    const float eo = has_up ? tag_o(v) : O;
+    nb.r = edge_lane ? er : nb.r;
+    nb.o = edge_lane ? eo : nb.o;
     return nb;
   };
   auto step = [&](int k, Nb nb) {  // column k from column k - 1, k >= 1
@@ -694,7 +720,10 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
 #ifdef DS2CTC_EXP_NOSTORE
     return;
 #endif
-    float* dst = cb_row(k, e) + 2 * K * ctid;
+    // threads without cells write a per-thread dummy slot instead (plain
+    // stores the scheduler can move, no branch, no predicate asm)
+    float* dst = stores ? cb_row(k, e) + 2 * K * ctid : sdummy + (2 * K + 4) * (ctid & 7);
+    float* odst = stores ? cb_row(k, e) + OB + ctid : dst + 2 * K;
     float v[2 * K];
 #pragma unroll
     for (int p = 0; p < K; ++p) {
@@ -704,17 +733,15 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
       v[2 * p] = dir == 0 ? cbv : clv;
       v[2 * p + 1] = dir == 0 ? clv : cbv;
     }
-    if (stores) {
-      if (K % 2 == 0) {
+    if (K % 2 == 0) {
 #pragma unroll
-        for (int q = 0; q < K / 2; ++q)
-          reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-      } else {
+      for (int q = 0; q < K / 2; ++q)
+        reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    } else {
 #pragma unroll
-        for (int p = 0; p < K; ++p) reinterpret_cast<float2*>(dst)[p] = make_float2(v[2 * p], v[2 * p + 1]);
-      }
-      (dst - 2 * K * ctid)[OB + ctid] = O;
+      for (int p = 0; p < K; ++p) reinterpret_cast<float2*>(dst)[p] = make_float2(v[2 * p], v[2 * p + 1]);
     }
+    *odst = O;
   };
 
   // Phase 2: label-cell occupancies from the partner's stored columns,
@@ -932,6 +959,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     cur = nxt;
     ++ep;
   }
+  MEET_STAMP(7);
   if (grad_warp && !dead && want_grad) grad_rows(prev);  // the last phase-2 epoch
 
   // ---- costs: fused cost = sum_t ls_t - log Z' (natural log; log Z' of the shifted frames) ----
@@ -944,6 +972,9 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     if (dir == 1) zero_rows(T, a.t_max);
   }
   cluster_barrier();
+#ifdef DS2CTC_EPOCH_TIMING
+  if (blockIdx.x < 2 && tid == 0) g_kernel_end[dir] = clock64();
+#endif
   if (dir == 0 && tid == 0) {
     a.logz[b] = logz2;
     if (fused) {
@@ -985,7 +1016,9 @@ extern "C" int ds2ctc_debug_epoch_clocks(long long* host) {
   return cudaMemcpyFromSymbol(host, g_epoch_clock, sizeof(g_epoch_clock));
 }
 extern "C" int ds2ctc_debug_meet_clocks(long long* host) {
-  return cudaMemcpyFromSymbol(host, g_meet_clock, sizeof(g_meet_clock));
+  int e = cudaMemcpyFromSymbol(host, g_meet_clock, sizeof(g_meet_clock));
+  if (e) return e;
+  return cudaMemcpyFromSymbol(host + 16, g_kernel_end, sizeof(g_kernel_end));
 }
 extern "C" int ds2ctc_debug_step_clocks(long long* host) {
   return cudaMemcpyFromSymbol(host, g_step_clock, sizeof(g_step_clock));

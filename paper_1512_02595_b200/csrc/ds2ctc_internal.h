@@ -61,6 +61,7 @@ struct Geometry {
   int off_xraw, off_emis, off_lse, off_el, off_tile, off_occ, off_bnd, off_meta, off_red;
   int off_cb;     // column buffer [2][P][cw_max] floats (TMA bulk stores / loads of lattice columns)
   int off_mbar;   // two mbarriers (one per column-buffer half)
+  int off_dummy;  // write sink for chain threads without cells
   int xstride;    // floats per xraw row (odd)
   int estride;    // floats per eb/el row (odd)
   int cw_max;     // floats per stored column (max over batch)
@@ -127,6 +128,7 @@ inline Geometry make_geometry(int max_L_all, int max_L, int max_nkey, int A, boo
     // position (L+1), symbol -> slot (A shorts, fused)
     g.off_meta = take(4 * (4 * max_L + 2 * max_nkey + 8) + (fused ? 2 * A : 0));
     g.off_red = take(8 * 72);
+    g.off_dummy = take(4 * 8 * (2 * g.K + 4));
     g.smem = off;
     if (static_cast<size_t>(off) <= kSmemBudget) break;
   }

@@ -69,10 +69,15 @@ def run(so, A=29, T=700, L=150, B=64, brief=False):
             print(f"  k+{k:2d} " + "  ".join(row))
     print("TIGHT cycles/step: critical", steps[0, 7, 31, 3] / 1000.0, "| + load_emis", steps[0, 7, 31, 2] / 1000.0,
           "| + stamps & real k", steps[0, 7, 31, 1] / 1000.0)
-    meet = np.zeros((2, 8), dtype=np.int64)
-    if lib.ds2ctc_debug_meet_clocks(meet.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong))) == 0:
+    meetbuf = np.zeros(18, dtype=np.int64)
+    if lib.ds2ctc_debug_meet_clocks(meetbuf.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong))) == 0:
+        meet = meetbuf[:16].reshape(2, 8)
         for cta in range(2):
             m = meet[cta]
+            e0 = buf[cta, 0, 0, 0]
+            last = max(int(buf[cta, e, w, 1]) for e in range(128) for w in range(33) if buf[cta, e, w, 1] > 0)
+            print(f"  cta{cta}: kernel: prologue {e0 - m[6]}, epochs {last - e0}, after-epochs {m[7] - last}, "
+                  f"tail {meetbuf[16 + cta] - m[7]}, total {meetbuf[16 + cta] - m[6]}")
             print(f"  cta{cta}: meet: store+wait {m[1]-m[0]}, cluster barrier {m[2]-m[1]}, logZ {m[3]-m[2]}, "
                   f"shift+load {m[4]-m[3]}, sync {m[5]-m[4]}")
     if brief:
