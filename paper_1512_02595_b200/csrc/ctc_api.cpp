@@ -145,17 +145,20 @@ std::pair<int, int> build_metadata(const Layout& lay, const int* flat_labels, co
   int* key_pos = blob.data() + lay.key_pos / 4;
   if (lay.sum_L > 0) std::memcpy(labels, flat_labels, sizeof(int) * lay.sum_L);
 
-  // Per-symbol scratch, reset lazily by a per-utterance stamp (no O(A) clear per utterance).
-  thread_local std::vector<unsigned> stamp;
-  thread_local std::vector<int> cnt, next;
-  thread_local unsigned epoch = 0;
-  if (static_cast<int>(stamp.size()) < A) {
-    stamp.assign(A, 0u);
-    cnt.assign(A, 0);
-    next.assign(A, 0);
+  // Per-symbol scratch (hoisted out of thread-local storage for the loops):
+  // a presence bitset over the alphabet (ascending symbol order by a word
+  // scan) and counts, both cleared after each utterance.
+  thread_local std::vector<uint64_t> bits_v;
+  thread_local std::vector<int> cnt_v, next_v;
+  const int nwords = (A + 63) / 64;
+  if (static_cast<int>(cnt_v.size()) < A) {
+    bits_v.assign(nwords, 0ull);
+    cnt_v.assign(A, 0);
+    next_v.assign(A, 0);
   }
-  std::vector<int> distinct;
-  distinct.reserve(256);
+  uint64_t* bits = bits_v.data();
+  int* cnt = cnt_v.data();
+  int* next = next_v.data();
 
   int max_L_all = 0;
   for (int b = 0; b < B; ++b) max_L_all = std::max(max_L_all, label_lengths[b]);
@@ -181,11 +184,11 @@ std::pair<int, int> build_metadata(const Layout& lay, const int* flat_labels, co
     // slot 0 = blank (all even lattice rows, plus label positions whose symbol
     // is the blank id), slots 1.. = distinct non-blank symbols ascending,
     // positions ascending within a slot. Counting sort by symbol.
-    if (++epoch == 0) {  // stamp wrap-around: clear once every 2^32 utterances
-      std::fill(stamp.begin(), stamp.end(), 0u);
-      epoch = 1;
-    }
-    distinct.clear();
+    int* kc = key_char + key_off;
+    int* ks = key_start + key_off + b;
+    int nkey = 1;
+    kc[0] = blank;
+    ks[0] = 0;
     int n_blank = 0;
     for (int i = 0; i < L; ++i) {
       const int sym = lab[i];
@@ -193,37 +196,28 @@ std::pair<int, int> build_metadata(const Layout& lay, const int* flat_labels, co
         ++n_blank;
         continue;
       }
-      if (stamp[sym] != epoch) {
-        stamp[sym] = epoch;
-        cnt[sym] = 0;
-        distinct.push_back(sym);
-      }
+      bits[sym >> 6] |= 1ull << (sym & 63);
       ++cnt[sym];
     }
-    std::sort(distinct.begin(), distinct.end());
-    const int nkey = 1 + static_cast<int>(distinct.size());
-    int* ks = key_start + key_off + b;
-    key_char[key_off] = blank;
-    ks[0] = 0;
     ks[1] = n_blank;
+    next[blank] = 0;
     int run = n_blank;
-    for (int j = 0; j < nkey - 1; ++j) {
-      const int sym = distinct[j];
-      key_char[key_off + 1 + j] = sym;
-      next[sym] = run;
-      run += cnt[sym];
-      ks[2 + j] = run;
+    for (int w = 0; w < nwords; ++w) {
+      uint64_t x = bits[w];
+      if (x == 0) continue;
+      bits[w] = 0;
+      do {
+        const int sym = w * 64 + __builtin_ctzll(x);
+        x &= x - 1;
+        kc[nkey] = sym;
+        next[sym] = run;
+        run += cnt[sym];
+        cnt[sym] = 0;
+        ks[++nkey] = run;
+      } while (x);
     }
     int* kp = key_pos + lab_off;
-    int nb = 0;
-    for (int i = 0; i < L; ++i) {
-      const int sym = lab[i];
-      if (sym == blank) kp[nb++] = i;
-      else kp[next[sym]++] = i;
-    }
-    // unused tail of this utterance's key CSR slots (nkey <= L + 1)
-    for (int j = nkey; j < L + 1; ++j) key_char[key_off + j] = 0;
-    for (int j = nkey + 1; j < L + 2; ++j) ks[j] = run;
+    for (int i = 0; i < L; ++i) kp[next[lab[i]]++] = i;
     u.nkey = nkey;
     if (u.status == 0) {
       max_L = std::max(max_L, L);
