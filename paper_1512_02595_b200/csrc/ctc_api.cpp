@@ -17,15 +17,6 @@
 #include "ds2ctc.h"
 #include "ds2ctc_internal.h"
 
-namespace ds2ctc {
-int k1_max_pairs() {
-  static const int v = [] {
-    const char* e = std::getenv("DS2CTC_K1_MAX_PAIRS");
-    return e ? std::atoi(e) : 96;
-  }();
-  return v;
-}
-}  // namespace ds2ctc
 
 namespace ds2ctc {
 namespace {

@@ -177,23 +177,12 @@ __device__ __forceinline__ void cp_async_wait() {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-// Tagged boundary values: residual r (32 bits) | offset O as a 24-bit
-// integer | the step's low 8 bits. An aligned 64-bit shared store is
-// single-copy atomic, so a reader that sees the tag sees the value.
-__device__ __forceinline__ unsigned long long tag_pack(float r, float o, int tag) {
-  const unsigned lo = (static_cast<unsigned>(__float2int_rn(o)) << 8) | (static_cast<unsigned>(tag) & 0xFFu);
-  return (static_cast<unsigned long long>(__float_as_uint(r)) << 32) | lo;
-}
-__device__ __forceinline__ float tag_r(unsigned long long u) { return __uint_as_float(static_cast<unsigned>(u >> 32)); }
-__device__ __forceinline__ float tag_o(unsigned long long u) {
-  return static_cast<float>(static_cast<int>(static_cast<unsigned>(u)) >> 8);
-}
-
-__device__ __forceinline__ void st_tagged(bool pred, unsigned long long* slot, float r, float o, int tag) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.volatile.shared.u64 [%0], %1;\n\t}" ::"r"(
-          smem_addr(slot)),
-      "l"(tag_pack(r, o, tag)), "r"(static_cast<unsigned>(pred)));
+// Halo refresh words: a value's 32 bits | the refresh number. An aligned
+// 64-bit shared store is single-copy atomic, so a reader that sees the tag
+// sees the value.
+__device__ __forceinline__ void st_word(unsigned long long* slot, float v, int tag) {
+  const unsigned long long w = (static_cast<unsigned long long>(__float_as_uint(v)) << 32) | static_cast<unsigned>(tag);
+  asm volatile("st.volatile.shared.u64 [%0], %1;" ::"r"(smem_addr(slot)), "l"(w));
 }
 
 // Watchdog: every spin-wait is bounded. A wait that exceeds the bound (a
@@ -214,20 +203,6 @@ __device__ __noinline__ void watchdog_fire(int kind, int step) {
 // Spin until the slot carries `tag`. Called warp-uniformly where possible.
 // Polls off the critical path back off with nanosleep so that spinning warps
 // do not crowd the shared-memory/shuffle (MIO) queue the recursion uses.
-// Spin until the slot carries `tag`; returns the raw tagged word.
-__device__ __forceinline__ unsigned long long ld_tagged(const unsigned long long* slot, int tag, int kind = 1) {
-  unsigned long long u;
-  for (unsigned n = 0;; ++n) {
-    asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(u) : "r"(smem_addr(slot)));
-    if ((u & 0xFFull) == (static_cast<unsigned long long>(tag) & 0xFFull)) break;
-    if (n == kSpinLimit) {
-      watchdog_fire(kind, tag);
-      break;
-    }
-  }
-  return u;
-}
-
 // Wait for phase `parity` of an mbarrier (bounded, like every wait here).
 __device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned parity) {
   for (unsigned n = 0;; ++n) {
@@ -336,7 +311,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   float* el = reinterpret_cast<float*>(smem + g.off_el);
   float* tile = reinterpret_cast<float*>(smem + g.off_tile);
   float* occs = reinterpret_cast<float*>(smem + g.off_occ);
-  unsigned long long* bnd = reinterpret_cast<unsigned long long*>(smem + g.off_bnd);
+  unsigned long long* ring = reinterpret_cast<unsigned long long*>(smem + g.off_ring);
   int* s_lab = reinterpret_cast<int*>(smem + g.off_meta);
   int* s_kchar = s_lab + (L + 1);
   int* s_kstart = s_kchar + u.nkey;
@@ -366,7 +341,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   for (int q = tid; q < L; q += NT) s_kpos[q] = a.key_pos[u.lab_off + q];
   if (fused)
     for (int c = tid; c < a.A; c += NT) s_slot[c] = -1;
-  for (int q = tid; q < NCW * P2; q += NT) bnd[q] = ~0ull;
+  for (int q = tid; q < NCW * g.ring_depth * kHaloLanes * (2 * K + 1); q += NT) ring[q] = ~0ull;
   if (tid == 0) {
     mbar_init(cb_mbar, 1);
     mbar_init(cb_mbar + 1, 1);
@@ -401,7 +376,12 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   const bool grad_warp = warp == NCW + 1;  // gradient / occupancy rows (SMSP 0 next to the service warp when NCW = 3)
   const bool is_chain = warp >= 1 && warp - 1 < nw_u;
   const int cwarp = is_chain ? warp - 1 : 0;  // chain-warp index
-  const int ctid = cwarp * 32 + lane;         // chain thread index
+  // Halo: the forward (backward) chain warp's first (last) kHaloLanes lanes
+  // recompute the upstream warp's edge lanes; the others own cells. ctid is
+  // the owner index of the lane's cells (stored-column thread index).
+  const bool halo_lane = dir == 0 ? lane < kHaloLanes : lane >= kOwnedLanes;
+  const int ctid = cwarp * kOwnedLanes + lane - (dir == 0 ? kHaloLanes : 0);
+  const bool owner = is_chain && !halo_lane && ctid >= 0;
 
   // Cells of this lane.
   bool has_b[K], has_l[K];
@@ -409,8 +389,8 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   for (int p = 0; p < K; ++p) {
     const int i = ctid * K + p;
     const int li = dir == 0 ? i : i - 1;  // label index of this pair's label cell
-    has_b[p] = is_chain && i <= L;
-    has_l[p] = is_chain && li >= 0 && li < L;
+    has_b[p] = owner && i <= L;
+    has_l[p] = owner && li >= 0 && li < L;
   }
 
   double logz2 = 0.0;
@@ -591,15 +571,18 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   // =====================================================================
   // Emission-row index of each cell; cells that do not exist read the
   // sentinel column (no predicate between the loads and their use).
+  // (halo lanes compute the same cells as their owners, so these ignore ownership)
   int sidx_b[K], sidx_l[K];
   bool skip[K];
 #pragma unroll
   for (int p = 0; p < K; ++p) {
     const int i = ctid * K + p;
     const int li = dir == 0 ? i : i - 1;
-    const int sym = has_l[p] ? s_lab[li] : a.blank;
-    sidx_l[p] = has_l[p] ? (fused ? sym : s_slotpos[li]) : g.SW;
-    sidx_b[p] = has_b[p] ? (fused ? a.blank : 0) : g.SW;
+    const bool eb = is_chain && i >= 0 && i <= L;
+    const bool ell = is_chain && li >= 0 && li < L;
+    const int sym = ell ? s_lab[li] : a.blank;
+    sidx_l[p] = ell ? (fused ? sym : s_slotpos[li]) : g.SW;
+    sidx_b[p] = eb ? (fused ? a.blank : 0) : g.SW;
     skip[p] = is_chain && i >= 1 && i < L && s_lab[i] != a.blank && s_lab[i] != s_lab[i - 1];
   }
   float vb[K], vl[K];  // carried residuals: alpha (forward) or emission-inclusive beta~ (backward)
@@ -635,17 +618,9 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
         vl[p] = last ? eL[p] : SENT;
       }
     }
-    if (dir == 0) st_tagged(lane == 31 && cwarp + 1 < nw_u, bnd + cwarp * P2, vl[K - 1], O, 0);
-    else st_tagged(lane == 0 && cwarp > 0, bnd + cwarp * P2, vl[0], O, 0);
   };
   // Neighbour cell for step k as (residual, offset): a shuffle inside the
-  // warp; across warps the tagged boundary slot, prefetched one step early
-  // (the upstream warp runs ahead: its boundary cell depends on the far side
-  // of the warp only K steps later), re-polled if stale.
-  unsigned long long bpre = ~0ull;
-  const int up_w = dir == 0 ? cwarp - 1 : cwarp + 1;  // upstream warp
-  // vote results are warp-uniform, so branches on them need no reconvergence
-  const bool has_up = __all_sync(0xffffffffu, up_w >= 0 && up_w < nw_u);
+  // warp. The warp's outer edge lane has no neighbour (the halo absorbs it).
   const bool edge_lane = lane == (dir == 0 ? 0 : 31);
   struct Nb {
     float r, o;
@@ -659,18 +634,9 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
       nb.r = __shfl_down_sync(0xffffffffu, vl[0], 1);
       nb.o = __shfl_down_sync(0xffffffffu, O, 1);
     }
-#ifdef DS2CTC_EXP_NOBND
-    if (edge_lane) nb = {SENT, O};
-    return nb;
-#endif
-    unsigned long long v = bpre;
-    const bool stale = (v & 0xFFull) != (static_cast<unsigned long long>(k - 1) & 0xFFull);
-    if (has_up && __any_sync(0xffffffffu, stale)) v = ld_tagged(bnd + up_w * P2 + ((k - 1) & M2), k - 1);
-    // selects, not a branch on the edge lane
-    const float er = has_up ? tag_r(v) : SENT;
-    const float eo = has_up ? tag_o(v) : O;
-    nb.r = edge_lane ? er : nb.r;
-    nb.o = edge_lane ? eo : nb.o;
+    nb.r = edge_lane ? SENT : nb.r;
+    nb.o = edge_lane ? O : nb.o;
+    (void)k;
     return nb;
   };
   auto step = [&](int k, Nb nb) {  // column k from column k - 1, k >= 1
@@ -707,15 +673,62 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
       }
     }
     O = live ? O + sh : nb.o;
-    const int down = dir == 0 ? cwarp + 1 : cwarp - 1;
-    if (dir == 0) st_tagged(lane == 31 && down < nw_u, bnd + cwarp * P2 + (k & M2), vl[K - 1], O, k);
-    else st_tagged(lane == 0 && down >= 0, bnd + cwarp * P2 + (k & M2), vl[0], O, k);
-    asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(bpre) : "r"(smem_addr(bnd + max(up_w, 0) * P2 + (k & M2))));
+    (void)k;
   };
+  // Halo refresh (every halo_steps(K) steps and at the meet): the upstream
+  // warp's edge lanes publish their carried cells, tagged with the refresh
+  // number, and this warp's halo lanes take them over. The only cross-warp
+  // wait of the recursion.
+  const int up_w = dir == 0 ? cwarp - 1 : cwarp + 1;
+  const bool publisher = is_chain && (dir == 0 ? lane >= kOwnedLanes && cwarp + 1 < nw_u : lane < kHaloLanes && cwarp > 0);
+  const bool consumer = is_chain && halo_lane && up_w >= 0 && up_w < nw_u;
+  const int hl = dir == 0 ? (lane >= kOwnedLanes ? lane - kOwnedLanes : lane) : (lane < kHaloLanes ? lane : lane - kOwnedLanes);
+  constexpr int HW = 2 * K + 1;  // words per lane: 2K residuals + the offset
+  int rc = 0;                    // refresh counter (identical in every warp)
+  auto refresh = [&]() {
+    ++rc;
+    const int slot = rc % g.ring_depth;
+    if (publisher) {
+      unsigned long long* dst = ring + ((static_cast<size_t>(cwarp) * g.ring_depth + slot) * kHaloLanes + hl) * HW;
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        st_word(dst + 2 * p, vb[p], rc);
+        st_word(dst + 2 * p + 1, vl[p], rc);
+      }
+      st_word(dst + 2 * K, O, rc);
+    }
+    if (consumer) {
+      const unsigned long long* src =
+          ring + ((static_cast<size_t>(up_w) * g.ring_depth + slot) * kHaloLanes + hl) * HW;
+      unsigned long long w[HW];
+      for (unsigned n = 0;; ++n) {
+        bool ok = true;
+#pragma unroll
+        for (int q = 0; q < HW; ++q) {
+          asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(w[q]) : "r"(smem_addr(src + q)));
+          ok &= static_cast<unsigned>(w[q]) == static_cast<unsigned>(rc);
+        }
+        if (ok) break;
+        if (n == kSpinLimit) {
+          watchdog_fire(1, rc);
+          break;
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        vb[p] = __uint_as_float(static_cast<unsigned>(w[2 * p] >> 32));
+        vl[p] = __uint_as_float(static_cast<unsigned>(w[2 * p + 1] >> 32));
+      }
+      O = __uint_as_float(static_cast<unsigned>(w[2 * K] >> 32));
+    }
+    __syncwarp();
+  };
+  const int RS = halo_steps(K);
+  int since = 0;  // steps since the last refresh
 
   // Phase 1: column k -> the stored half-lattice: the residuals in slot
   // order and the thread's offset (value = offset + residual).
-  const bool stores = is_chain && ctid < column_threads(L, K);
+  const bool stores = owner && ctid < column_threads(L, K);
   auto store_column = [&](int k, const Epoch& e) {
 #ifdef DS2CTC_EXP_NOSTORE
     return;
@@ -777,7 +790,8 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   };
 
   // Steps [k0, k1) of one epoch. Step k computes column k and finishes
-  // column k - 1; the epoch's last column is finished after the loop.
+  // column k - 1; the epoch's last column is finished after the loop. The
+  // steps run in chunks between halo refreshes, without any cross-warp wait.
   unsigned cb_parity = 0;  // phase bits of the two column-buffer mbarriers
   auto chain_epoch = [&](const Epoch& e) {
     const bool ph2 = e.phase == 2;
@@ -787,29 +801,47 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     }
     load_emis(e.k0);
     STEP_STAMP(e.k0, e, 0);
-    if (!ph2 && e.k0 == 0) first_column();
-    else if (!ph2 || e.k0 > kmid) step(e.k0, neighbour(e.k0));  // the forward CTA's phase 2 starts at kmid
+    if (!ph2 && e.k0 == 0) {
+      first_column();
+    } else if (!ph2 || e.k0 > kmid) {  // the forward CTA's phase 2 starts at kmid
+      step(e.k0, neighbour(e.k0));
+      if (++since == RS) {
+        refresh();
+        since = 0;
+      }
+    }
     load_emis(e.k0 + 1);
     STEP_STAMP(e.k0, e, 2);
-    if (ph2) {
-      for (int k = e.k0 + 1; k < e.k1; ++k) {
-        STEP_STAMP(k, e, 0);
-        const Nb nb = neighbour(k);
-        occupancy_column(k - 1, e);
-        step(k, nb);
-        load_emis(k + 1);
-        STEP_STAMP(k, e, 2);
+    for (int k = e.k0 + 1; k < e.k1;) {
+      const int kb = min(e.k1, k + (RS - since));
+      since += kb - k;
+      if (ph2) {
+        for (; k < kb; ++k) {
+          STEP_STAMP(k, e, 0);
+          const Nb nb = neighbour(k);
+          occupancy_column(k - 1, e);
+          step(k, nb);
+          load_emis(k + 1);
+          STEP_STAMP(k, e, 2);
+        }
+      } else {
+        for (; k < kb; ++k) {
+          STEP_STAMP(k, e, 0);
+          const Nb nb = neighbour(k);
+          store_column(k - 1, e);
+          step(k, nb);
+          load_emis(k + 1);
+          STEP_STAMP(k, e, 2);
+        }
       }
+      if (since == RS) {
+        refresh();
+        since = 0;
+      }
+    }
+    if (ph2) {
       occupancy_column(e.k1 - 1, e);
     } else {
-      for (int k = e.k0 + 1; k < e.k1; ++k) {
-        STEP_STAMP(k, e, 0);
-        const Nb nb = neighbour(k);
-        store_column(k - 1, e);
-        step(k, nb);
-        load_emis(k + 1);
-        STEP_STAMP(k, e, 2);
-      }
       store_column(e.k1 - 1, e);
       fence_async_shared();  // the service warp bulk-stores this epoch's columns
     }
@@ -943,9 +975,8 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
           xb[p] -= zf;
           xl[p] -= zf;
         }
-        if (dir == 0) st_tagged(lane == 31 && cwarp + 1 < nw_u, bnd + cwarp * P2 + (kmid & M2), vl[K - 1], O, kmid);
-        else st_tagged(lane == 0 && cwarp > 0, bnd + cwarp * P2 + (kmid & M2), vl[0], O, kmid);
-        bpre = ~0ull;
+        refresh();  // the halo lanes take over the shifted upstream edge cells
+        since = 0;
       }
       if (service && lane == 0) {
         fence_async_all();  // the partner's bulk stores (ordered by the cluster barrier) -> our bulk loads

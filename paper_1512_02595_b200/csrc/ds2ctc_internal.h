@@ -26,7 +26,7 @@ namespace ds2ctc {
 
 constexpr int kMaxStates = 4095;  // == DS2CTC_MAX_STATES
 constexpr int kFusedMaxAlphabet = 128;
-constexpr int kMaxThreads = 320;  // <= 8 chain warps (K = 8, L <= 2047) + service + gradient warps
+constexpr int kMaxThreads = 384;  // <= 10 chain warps (K = 8, L <= 2047) + service + gradient warps
 constexpr size_t kAlign = 256;
 constexpr size_t kSmemBudget = 220 * 1024;
 
@@ -58,7 +58,8 @@ struct Geometry {
   int max_L;
   int fused;
   // shared-memory carve-up (bytes, 16-aligned)
-  int off_xraw, off_emis, off_lse, off_el, off_tile, off_occ, off_bnd, off_meta, off_red;
+  int off_xraw, off_emis, off_lse, off_el, off_tile, off_occ, off_ring, off_meta, off_red;
+  int ring_depth; // halo refresh ring entries per chain warp
   int off_cb;     // column buffer [2][P][cw_max] floats (TMA bulk stores / loads of lattice columns)
   int off_mbar;   // two mbarriers (one per column-buffer half)
   int off_dummy;  // write sink for chain threads without cells
@@ -70,18 +71,24 @@ struct Geometry {
   int smem;       // total bytes
 };
 
-DS2CTC_HD inline int chain_warps_for(int L, int K) { return (L + 1 + 32 * K - 1) / (32 * K); }
+// Chain warps: 32 lanes, of which kHaloLanes recompute the upstream warp's
+// edge lanes (refreshed every halo_steps(K) steps) and kOwnedLanes own cells.
+constexpr int kHaloLanes = 4;
+constexpr int kOwnedLanes = 32 - kHaloLanes;
+// The halo absorbs the wrong outer neighbour for 2*kHaloLanes*K rows, i.e.
+// kHaloLanes*K steps (the recursion moves 2 rows per step).
+DS2CTC_HD inline int halo_steps(int K) { return kHaloLanes * K < 16 ? kHaloLanes * K : 16; }
+DS2CTC_HD inline int column_threads(int L, int K);
+DS2CTC_HD inline int chain_warps_for(int L, int K) { return (column_threads(L, K) + kOwnedLanes - 1) / kOwnedLanes; }
 
 // Label pairs per chain thread. At most three chain warps while K <= 8, so
 // the service warp keeps an SM sub-partition (SMSP) of its own; each pair
 // costs 5 MUFU ops per step, so K also bounds the per-SMSP MUFU load.
 constexpr int kPairChoices[] = {1, 2, 3, 4, 6, 8};
-int k1_max_pairs();  // ctc_api.cpp (tunable: DS2CTC_K1_MAX_PAIRS)
 inline int pick_K(int max_L) {
   const int pairs = max_L + 1;
-  if (pairs <= k1_max_pairs()) return 1;
   for (int K : kPairChoices)
-    if (pairs <= 96 * K) return K;
+    if (pairs <= 3 * kOwnedLanes * K) return K;
   return 8;
 }
 
@@ -121,7 +128,8 @@ inline Geometry make_geometry(int max_L_all, int max_L, int max_nkey, int A, boo
     g.off_el = take(4 * 2 * P * g.estride);
     g.off_tile = take(4 * 32 * g.tstride);  // one row per service lane (all 32 lanes run, P <= 32)
     g.off_occ = take(4 * 32 * g.ostride);
-    g.off_bnd = take(8 * g.nchain * 2 * P);
+    g.ring_depth = 2 * (P / halo_steps(g.K) + 2);
+    g.off_ring = take(8 * g.nchain * g.ring_depth * kHaloLanes * (2 * g.K + 1));
     g.off_cb = take(4 * 2 * P * g.cw_max);
     g.off_mbar = take(16);
     // meta: labels (L+1), key_char (nkey), key_start (nkey+1), key_pos (L), slot of each label
