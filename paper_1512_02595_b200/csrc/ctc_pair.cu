@@ -500,7 +500,8 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     int q = s_kstart[1];
     for (; q + 3 < L; q += 4) {
       const int w0 = s_kq[q], w1 = s_kq[q + 1], w2 = s_kq[q + 2], w3 = s_kq[q + 3];
-      const float v0 = elr[w0 & 0xFFFF], v1 = elr[w1 & 0xFFFF], v2 = elr[w2 & 0xFFFF], v3 = elr[w3 & 0xFFFF];
+      const float v0 = ex2(elr[w0 & 0xFFFF]), v1 = ex2(elr[w1 & 0xFFFF]), v2 = ex2(elr[w2 & 0xFFFF]),
+                  v3 = ex2(elr[w3 & 0xFFFF]);
       const int j0 = w0 >> 16, j1 = w1 >> 16, j2 = w2 >> 16, j3 = w3 >> 16;
       if (j0 != cur) { oc[cur] = acc; tot += acc; acc = 0.f; cur = j0; }
       acc += v0;
@@ -515,7 +516,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
       const int w0 = s_kq[q];
       const int j0 = w0 >> 16;
       if (j0 != cur) { oc[cur] = acc; tot += acc; acc = 0.f; cur = j0; }
-      acc += elr[w0 & 0xFFFF];
+      acc += ex2(elr[w0 & 0xFFFF]);
     }
     if (u.nkey > 1) {
       oc[cur] = acc;
@@ -769,23 +770,36 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   for (int p = 0; p < K; ++p) pslot[p] = max(2 * K * ctid + 2 * p + (dir == 0 ? 2 : -1), 0);
   const int poff_lo = OB + max(dir == 0 ? ctid : ctid - 1, 0);  // writer threads of the first / last slot
   const int poff_hi = OB + (dir == 0 ? ctid + 1 : ctid);
+  // The partner cells of the next row are fetched one step ahead.
+  float pd[K], po_lo = 0.f, po_hi = 0.f;
+#pragma unroll
+  for (int p = 0; p < K; ++p) pd[p] = SENT;
+  auto partner_fetch = [&](int k, const Epoch& e) {
+    const float* row = cb_row(k, e);
+#pragma unroll
+    for (int p = 0; p < K; ++p) pd[p] = row[pslot[p]];
+    po_lo = row[poff_lo];
+    po_hi = row[poff_hi];
+  };
+  // gamma = alpha + beta - log Z (plain add, ctc.cpp:200), in log2 units; the
+  // carried offset was shifted by -log Z at the meet, so the offsets add
+  // exactly and only the residuals round. The gradient warp exponentiates.
   auto occupancy_column = [&](int k, const Epoch& e) {
 #ifdef DS2CTC_EXP_NOOCC
     return;
 #endif
-    const float* row = cb_row(k, e);
-    // gamma = alpha + beta - log Z (plain add, ctc.cpp:200); the carried
-    // offset was shifted by -log Z at the meet, so the offsets add exactly
-    // and only the residuals round.
-    const float o_lo = row[poff_lo] + O, o_hi = row[poff_hi] + O;
+    const float o_lo = po_lo + O, o_hi = po_hi + O;
+    float d[K];
+#pragma unroll
+    for (int p = 0; p < K; ++p) d[p] = pd[p];
+    partner_fetch(min(k + 1, e.k1 - 1), e);
     float* elr = el + (k & M2) * g.estride;
 #pragma unroll
     for (int p = 0; p < K; ++p) {
       const int i = ctid * K + p;
       const float rl = dir == 0 ? vl[p] : xl[p];
       const float ol = (dir == 0 ? p == K - 1 : p != 0) ? o_hi : o_lo;
-      const float o_l = ex2(ol + (rl + row[pslot[p]]));
-      if (has_l[p]) elr[dir == 0 ? i : i - 1] = o_l;
+      if (has_l[p]) elr[dir == 0 ? i : i - 1] = ol + (rl + d[p]);
     }
   };
 
@@ -798,6 +812,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     if (ph2) {  // this epoch's partner columns have landed
       mbar_wait(cb_mbar + (ep & 1), (cb_parity >> (ep & 1)) & 1u);
       cb_parity ^= 1u << (ep & 1);
+      partner_fetch(e.k0, e);
     }
     load_emis(e.k0);
     STEP_STAMP(e.k0, e, 0);
