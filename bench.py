@@ -344,7 +344,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": wl["scaling"],
-            "vs_baseline": None, "dtype": "f32 in/out, f64 lattice carry", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.workload, "desc": wl["desc"], "alphabet": A,
                        "global_batch": total_utts, "frames_per_step": total_frames,
                        "parallelism": f"dp{world}", "l2": "flushed between steps (256 MiB memset)"},
