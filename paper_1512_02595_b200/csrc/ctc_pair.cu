@@ -596,12 +596,20 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     eB[p] = eL[p] = SENT;
   }
 
+  // per-lane shared-memory addresses of the cells' emissions within a row;
+  // the row base is warp-uniform
+  unsigned eaddr_b[K], eaddr_l[K];
+#pragma unroll
+  for (int p = 0; p < K; ++p) {
+    eaddr_b[p] = smem_addr(emis + sidx_b[p]);
+    eaddr_l[p] = smem_addr(emis + sidx_l[p]);
+  }
   auto load_emis = [&](int k) {
-    const float* er = emis + (k & M2) * SW;
+    const unsigned row = static_cast<unsigned>((k & M2) * SW * 4);
 #pragma unroll
     for (int p = 0; p < K; ++p) {
-      eB[p] = er[sidx_b[p]];
-      eL[p] = er[sidx_l[p]];
+      asm("ld.shared.f32 %0, [%1];" : "=f"(eB[p]) : "r"(eaddr_b[p] + row));
+      asm("ld.shared.f32 %0, [%1];" : "=f"(eL[p]) : "r"(eaddr_l[p] + row));
     }
   };
   auto first_column = [&]() {
@@ -660,7 +668,9 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
 #pragma unroll
     for (int p = 1; p < K; ++p) mx = fmaxf(mx, fmaxf(nvb[p], nvl[p]));
     const bool live = mx > SENT_CUT;
-    const float sh = live ? rintf(mx) : 0.f;
+    // round to an integer by the 1.5 * 2^23 trick (two adds on the FMA pipe
+    // instead of FRND); exact for |mx| < 2^22, and dead threads use 0
+    const float sh = live ? __fsub_rn(__fadd_rn(mx, 12582912.f), 12582912.f) : 0.f;
 #pragma unroll
     for (int p = 0; p < K; ++p) {
       if (dir == 0) {
