@@ -676,11 +676,11 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
       if (dir == 0) {
         vb[p] = nvb[p] - sh;
         vl[p] = nvl[p] - sh;
-      } else {
+      } else {  // the carried value does not wait for the stored one
         xb[p] = nvb[p] - sh;
         xl[p] = nvl[p] - sh;
-        vb[p] = xb[p] + eB[p];
-        vl[p] = xl[p] + eL[p];
+        vb[p] = (nvb[p] + eB[p]) - sh;
+        vl[p] = (nvl[p] + eL[p]) - sh;
       }
     }
     O = live ? O + sh : nb.o;
