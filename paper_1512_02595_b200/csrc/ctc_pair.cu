@@ -734,7 +734,11 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     }
     __syncwarp();
   };
+#ifdef DS2CTC_EXP_NOREFRESH
+  const int RS = 1 << 30;
+#else
   const int RS = halo_steps(K);
+#endif
   int since = 0;  // steps since the last refresh
 
   // Phase 1: column k -> the stored half-lattice: the residuals in slot
@@ -820,7 +824,9 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   auto chain_epoch = [&](const Epoch& e) {
     const bool ph2 = e.phase == 2;
     if (ph2) {  // this epoch's partner columns have landed
+#ifndef DS2CTC_EXP_NOLOAD
       mbar_wait(cb_mbar + (ep & 1), (cb_parity >> (ep & 1)) & 1u);
+#endif
       cb_parity ^= 1u << (ep & 1);
       partner_fetch(e.k0, e);
     }
@@ -904,7 +910,9 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
 #endif
       if (lane == 0) {
         if (cur.phase == 1 && ep > 0) store_epoch(prev, (ep - 1) & 1);
+#ifndef DS2CTC_EXP_NOLOAD
         if (cur.phase == 2 && nxt.phase == 2) load_epoch(nxt, (ep + 1) & 1);
+#endif
       }
       stage(stg);
 #ifdef DS2CTC_EPOCH_TIMING
@@ -1005,7 +1013,9 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
       }
       if (service && lane == 0) {
         fence_async_all();  // the partner's bulk stores (ordered by the cluster barrier) -> our bulk loads
+#ifndef DS2CTC_EXP_NOLOAD
         load_epoch(nxt, (ep + 1) & 1);
+#endif
       }
       MEET_STAMP(4);
       __syncthreads();
