@@ -232,12 +232,20 @@ __device__ long long g_kernel_end[2];
   do {                \
     if (blockIdx.x < 2 && tid == 0) g_meet_clock[dir][i] = clock64(); \
   } while (0)
+// per-step stamps perturb the loop they measure (a divergent lane-0 branch per
+// stamp); they are compiled only with DS2CTC_STEP_STAMPS
+#ifdef DS2CTC_STEP_STAMPS
 #define STEP_STAMP(k, e, pt)                                                                            \
   do {                                                                                                  \
     if (blockIdx.x < 2 && lane == 0 && warp < 7 && (e).phase == 2 && (e).k0 == k2s + 2 * P &&           \
         (k) - (e).k0 < 32)                                                                              \
       g_step_clock[dir][warp][(k) - (e).k0][pt] = clock64();                                            \
   } while (0)
+#else
+#define STEP_STAMP(k, e, pt) \
+  do {                       \
+  } while (0)
+#endif
 #else
 #define STEP_STAMP(k, e, pt) \
   do {                       \
@@ -299,7 +307,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   const int OB = column_offsets_base(L, K);  // per-thread offsets of a stored column start here
   const int cw = u.col_w;
   const int nw_u = chain_warps_for(L, K);  // chain warps this utterance uses
-  const int SW = g.SW + 1;  // emission row: staged symbols + the sentinel column g.SW
+  const int SW = emis_stride(g.SW);  // emission row: staged symbols + the sentinel column g.SW (odd stride)
   const int nstage = fused ? a.A : u.nkey;
   const int kmid = dir == 0 ? tm : T - 1 - tm;
   const int k2s = dir == 0 ? kmid : kmid + 1;     // first phase-2 step (gradient rows)
@@ -399,14 +407,6 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   // =====================================================================
   // Service warp: staging / emissions / statistics / gradient rows.
   // =====================================================================
-  // Flat (frame, symbol) loops over a whole epoch: idx -> (idx / nstage,
-  // idx % nstage) by a multiply-high with a rounded-up reciprocal (exact for
-  // idx < 2^16 and nstage < 2^16).
-  const unsigned recip = static_cast<unsigned>((0x100000000ull + nstage - 1) / nstage);
-  auto split_idx = [&](int idx, int& r, int& c) {
-    r = static_cast<int>(__umulhi(static_cast<unsigned>(idx), recip));
-    c = idx - r * nstage;
-  };
   const float* xb_utt = a.x + static_cast<size_t>(b) * a.A;
   // Column-buffer bulk copies (TMA, issued by service lane 0).
   float* gcols = a.store + u.store_off;
@@ -428,23 +428,29 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   };
   auto stage = [&](const Epoch& e) {
     if (e.phase == 0) return;
-    const int total = (e.k1 - e.k0) * nstage;
+    // one frame row per iteration, lane = symbol: each row is one contiguous
+    // (coalesced) read of the utterance's logits
+    const int n = e.k1 - e.k0;
+    for (int c0 = 0; c0 < nstage; c0 += 32) {
+      const int c = c0 + lane;
+      if (c >= nstage) break;
+      const float* src = xb_utt + (fused ? c : s_kchar[c]);
 #pragma unroll 4
-    for (int idx = lane; idx < total; idx += 32) {
-      int r, c;
-      split_idx(idx, r, c);
-      const int k = e.k0 + r;
-      cp_async4(xraw + (k & MX) * g.xstride + c,
-                xb_utt + static_cast<size_t>(frame(k)) * rs + (fused ? c : s_kchar[c]));
+      for (int r = 0; r < n; ++r) {
+        const int k = e.k0 + r;
+        cp_async4(xraw + (k & MX) * g.xstride + c, src + static_cast<size_t>(frame(k)) * rs);
+      }
     }
     cp_async_commit();
   };
-  // After the staged rows landed: per-frame shift mk_t (max over the staged
-  // symbols), log-sum-exp (fused), and the shifted double-float emissions.
+  // After the staged rows landed (lane = frame): per-frame shift mk_t (max
+  // over the staged symbols), the shifted emissions (x - mk_t) * log2(e) and,
+  // fused, the log-sum-exp of the whole row in the same pass
+  // (log_softmax_rows, ctc.cpp:24-37).
   auto convert = [&](const Epoch& e) {
     if (e.phase == 0) return;
     const int n = e.k1 - e.k0;
-    if (lane < n) {  // lane = frame
+    if (lane < n) {
       const int k = e.k0 + lane;
       const float* xr = xraw + (k & MX) * g.xstride;
       float m0 = NEGF, m1 = NEGF;
@@ -456,29 +462,21 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
       if (c < nstage) m0 = fmaxf(m0, xr[c]);
       float mk = fmaxf(m0, m1);
       if (mk == NEGF) mk = 0.f;  // every staged symbol impossible: any shift works
-      float ls = 0.f;
-      if (fused) {  // log_softmax_rows statistics (ctc.cpp:24-37)
-        float s0 = 0.f, s1 = 0.f;
-        for (c = 0; c + 1 < a.A; c += 2) {
-          s0 += ex2((xr[c] - mk) * kL2eH);
-          s1 += ex2((xr[c + 1] - mk) * kL2eH);
-        }
-        if (c < a.A) s0 += ex2((xr[c] - mk) * kL2eH);
-        ls = lg2(s0 + s1) * kLn2f;
+      float* er = emis + (k & M2) * SW;
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll 4
+      for (c = 0; c < nstage; ++c) {
+        const float ev = emis_log2(xr[c], mk);
+        er[c] = ev;
+        if (c & 1) s1 += ex2(ev);  // ex2(sentinel) = 0
+        else s0 += ex2(ev);
       }
+      er[g.SW] = SENT;
+      const float ls = fused ? lg2(s0 + s1) * kLn2f : 0.f;
       lser[k & MX] = make_float2(mk, ls);
       if (k <= kcount) part_acc += fused ? static_cast<double>(ls) : -static_cast<double>(mk);
     }
-    if (lane < n) emis[((e.k0 + lane) & M2) * SW + g.SW] = SENT;
     __syncwarp();
-    const int total = n * nstage;
-#pragma unroll 4
-    for (int idx = lane; idx < total; idx += 32) {
-      int r, c;
-      split_idx(idx, r, c);
-      const int k = e.k0 + r;
-      emis[(k & M2) * SW + c] = emis_log2(xraw[(k & MX) * g.xstride + c], lser[k & MX].x);
-    }
   };
   // Gradient rows of a finished phase-2 epoch, lane = row (ctc.cpp:196-203,
   // 69-79). All lanes walk the same (uniform) index sequences, so every loop
@@ -500,8 +498,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     int q = s_kstart[1];
     for (; q + 3 < L; q += 4) {
       const int w0 = s_kq[q], w1 = s_kq[q + 1], w2 = s_kq[q + 2], w3 = s_kq[q + 3];
-      const float v0 = ex2(elr[w0 & 0xFFFF]), v1 = ex2(elr[w1 & 0xFFFF]), v2 = ex2(elr[w2 & 0xFFFF]),
-                  v3 = ex2(elr[w3 & 0xFFFF]);
+      const float v0 = elr[w0 & 0xFFFF], v1 = elr[w1 & 0xFFFF], v2 = elr[w2 & 0xFFFF], v3 = elr[w3 & 0xFFFF];
       const int j0 = w0 >> 16, j1 = w1 >> 16, j2 = w2 >> 16, j3 = w3 >> 16;
       if (j0 != cur) { oc[cur] = acc; tot += acc; acc = 0.f; cur = j0; }
       acc += v0;
@@ -516,7 +513,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
       const int w0 = s_kq[q];
       const int j0 = w0 >> 16;
       if (j0 != cur) { oc[cur] = acc; tot += acc; acc = 0.f; cur = j0; }
-      acc += ex2(elr[w0 & 0xFFFF]);
+      acc += elr[w0 & 0xFFFF];
     }
     if (u.nkey > 1) {
       oc[cur] = acc;
@@ -537,22 +534,18 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
       for (int j = 0; j < u.nkey; ++j) tr[j] = oc[j];
     }
     __syncwarp();
-    const int total = n * nstage;  // fused: nstage == A; split: nstage == nkey
+    // one row per iteration, lane = symbol: coalesced row stores
     if (fused) {
       float* gb = a.grad + static_cast<size_t>(b) * a.A;
+      for (int c = lane; c < a.A; c += 32) {
 #pragma unroll 4
-      for (int idx = lane; idx < total; idx += 32) {
-        int r, c;
-        split_idx(idx, r, c);
-        gb[static_cast<size_t>(frame(e.k0 + r)) * rs + c] = tile[r * g.tstride + c];
+        for (int r = 0; r < n; ++r) gb[static_cast<size_t>(frame(e.k0 + r)) * rs + c] = tile[r * g.tstride + c];
       }
     } else {
       float* ob = a.occ + u.occ_off;
+      for (int c = lane; c < u.nkey; c += 32) {
 #pragma unroll 4
-      for (int idx = lane; idx < total; idx += 32) {
-        int r, c;
-        split_idx(idx, r, c);
-        ob[static_cast<size_t>(frame(e.k0 + r)) * u.nkey + c] = tile[r * g.tstride + c];
+        for (int r = 0; r < n; ++r) ob[static_cast<size_t>(frame(e.k0 + r)) * u.nkey + c] = tile[r * g.tstride + c];
       }
     }
     __syncwarp();
@@ -696,11 +689,15 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   const int hl = dir == 0 ? (lane >= kOwnedLanes ? lane - kOwnedLanes : lane) : (lane < kHaloLanes ? lane : lane - kOwnedLanes);
   constexpr int HW = 2 * K + 1;  // words per lane: 2K residuals + the offset
   int rc = 0;                    // refresh counter (identical in every warp)
+  const int ring_mask = g.ring_depth - 1;  // power of two
+  unsigned long long* const ring_pub = ring + (static_cast<size_t>(cwarp) * g.ring_depth * kHaloLanes + hl) * HW;
+  const unsigned long long* const ring_sub =
+      ring + (static_cast<size_t>(max(up_w, 0)) * g.ring_depth * kHaloLanes + hl) * HW;
   auto refresh = [&]() {
     ++rc;
-    const int slot = rc % g.ring_depth;
+    const int slot_off = (rc & ring_mask) * kHaloLanes * HW;
     if (publisher) {
-      unsigned long long* dst = ring + ((static_cast<size_t>(cwarp) * g.ring_depth + slot) * kHaloLanes + hl) * HW;
+      unsigned long long* dst = ring_pub + slot_off;
 #pragma unroll
       for (int p = 0; p < K; ++p) {
         st_word(dst + 2 * p, vb[p], rc);
@@ -709,8 +706,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
       st_word(dst + 2 * K, O, rc);
     }
     if (consumer) {
-      const unsigned long long* src =
-          ring + ((static_cast<size_t>(up_w) * g.ring_depth + slot) * kHaloLanes + hl) * HW;
+      const unsigned long long* src = ring_sub + slot_off;
       unsigned long long w[HW];
       for (unsigned n = 0;; ++n) {
         bool ok = true;
@@ -782,6 +778,9 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   int pslot[K];
 #pragma unroll
   for (int p = 0; p < K; ++p) pslot[p] = max(2 * K * ctid + 2 * p + (dir == 0 ? 2 : -1), 0);
+  int el_idx[K];  // occupancy-row index of each label cell (L = the spare slot, never read)
+#pragma unroll
+  for (int p = 0; p < K; ++p) el_idx[p] = has_l[p] ? (dir == 0 ? ctid * K + p : ctid * K + p - 1) : L;
   const int poff_lo = OB + max(dir == 0 ? ctid : ctid - 1, 0);  // writer threads of the first / last slot
   const int poff_hi = OB + (dir == 0 ? ctid + 1 : ctid);
   // The partner cells of the next row are fetched one step ahead.
@@ -797,7 +796,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   };
   // gamma = alpha + beta - log Z (plain add, ctc.cpp:200), in log2 units; the
   // carried offset was shifted by -log Z at the meet, so the offsets add
-  // exactly and only the residuals round. The gradient warp exponentiates.
+  // exactly and only the residuals round; the occupancy row holds 2^gamma.
   auto occupancy_column = [&](int k, const Epoch& e) {
 #ifdef DS2CTC_EXP_NOOCC
     return;
@@ -810,10 +809,10 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     float* elr = el + (k & M2) * g.estride;
 #pragma unroll
     for (int p = 0; p < K; ++p) {
-      const int i = ctid * K + p;
       const float rl = dir == 0 ? vl[p] : xl[p];
       const float ol = (dir == 0 ? p == K - 1 : p != 0) ? o_hi : o_lo;
-      if (has_l[p]) elr[dir == 0 ? i : i - 1] = ol + (rl + d[p]);
+      // linear occupancy 2^gamma; unconditional: cells without a label write the row's spare slot L
+      elr[el_idx[p]] = ex2(ol + (rl + d[p]));
     }
   };
 
@@ -992,6 +991,10 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
         logz2 = M + log2(tot);
       }
       dead = logz2 == -__builtin_huge_val();  // zero-probability lattice (ctc.cpp:189-193)
+#ifdef DS2CTC_EXP_NOREFRESH
+      dead = false;  // timing experiment: the unrefreshed halo makes garbage
+      if (!(logz2 > -1e30 && logz2 < 1e30)) logz2 = 0.0;
+#endif
       MEET_STAMP(3);
       if (dead || !want_grad) break;
       if (is_chain) {

@@ -49,6 +49,10 @@ static_assert(sizeof(UttDesc) == 64, "UttDesc layout");
 
 DS2CTC_HD inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
+// Floats per emission row: the staged symbols, the sentinel column (index SW)
+// and padding to an odd stride (rows indexed by frame are bank-conflict free).
+DS2CTC_HD inline int emis_stride(int SW) { return (SW + 1) | 1; }
+
 // Launch geometry shared by every utterance of one call.
 struct Geometry {
   int K;          // label pairs per chain thread
@@ -123,12 +127,13 @@ inline Geometry make_geometry(int max_L_all, int max_L, int max_nkey, int A, boo
     };
     const int RX = 4 * P;
     g.off_xraw = take(4 * RX * g.xstride);
-    g.off_emis = take(4 * 2 * P * (g.SW + 1));  // + a sentinel column for cells that do not exist
+    g.off_emis = take(4 * 2 * P * emis_stride(g.SW));  // + a sentinel column for cells that do not exist
     g.off_lse = take(8 * RX);
     g.off_el = take(4 * 2 * P * g.estride);
     g.off_tile = take(4 * 32 * g.tstride);  // one row per service lane (all 32 lanes run, P <= 32)
     g.off_occ = take(4 * 32 * g.ostride);
-    g.ring_depth = 2 * (P / halo_steps(g.K) + 2);
+    g.ring_depth = 4;  // a power of two >= 2 * (P / halo_steps + 2): the slot is a mask, not a division
+    while (g.ring_depth < 2 * (P / halo_steps(g.K) + 2)) g.ring_depth *= 2;
     g.off_ring = take(8 * g.nchain * g.ring_depth * kHaloLanes * (2 * g.K + 1));
     g.off_cb = take(4 * 2 * P * g.cw_max);
     g.off_mbar = take(16);

@@ -6,6 +6,8 @@
 //   V=0 lse2 + lse3 (the product kernel's arithmetic, 5 MUFU per pair)
 //   V=1 lse2 + lse2 (label cell = lse2(label, skip ? blank_lse : blank), 4 MUFU)
 //   V=2 as 1, re-centring shift lagged by one step (applied with the emission)
+//   V=3 linear-in-step: one ex2 per cell, sums in linear, one lg2 per cell (4 MUFU per pair + 1)
+//   V=4 as 3 + a per-step fragility vote (any live cell below -100 -> exact step)
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 chain_step.cu
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -54,11 +56,23 @@ __global__ void __launch_bounds__(128, 1) kstep(int T, float* out, long long* cy
     no = lane == 0 ? O : no;
     const float n0 = nr + (no - O);
     float nvb[K], nvl[K];
-    if (V == 2) {
+    if (V >= 2) {
       eb -= shp;
 #pragma unroll
       for (int p = 0; p < K; ++p) el[p] -= shp;
     }
+    if (V >= 3) {
+      float Eb[K], El[K];
+#pragma unroll
+      for (int p = 0; p < K; ++p) { Eb[p] = ex2(vb[p]); El[p] = ex2(vl[p]); }
+      const float En = ex2(n0);
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        const float n1 = p == 0 ? En : El[p - 1];
+        nvb[p] = lg2(Eb[p] + n1) + eb;
+        nvl[p] = lg2(fmaf(skip[p] ? 1.f : 0.f, n1, El[p]) + Eb[p]) + el[p];
+      }
+    } else
 #pragma unroll
     for (int p = 0; p < K; ++p) {
       const float n1 = p == 0 ? n0 : vl[p - 1];
@@ -73,7 +87,13 @@ __global__ void __launch_bounds__(128, 1) kstep(int T, float* out, long long* cy
 #pragma unroll
     for (int p = 1; p < K; ++p) mx = fmaxf(mx, fmaxf(nvb[p], nvl[p]));
     const float sh = __fsub_rn(__fadd_rn(mx, 12582912.f), 12582912.f);
-    if (V == 2) {
+    if (V == 4) {
+      bool frag = n0 < -100.f && n0 > -1e29f;
+#pragma unroll
+      for (int p = 0; p < K; ++p) frag |= (nvb[p] - mx < -100.f && nvb[p] > -1e29f) | (nvl[p] - mx < -100.f && nvl[p] > -1e29f);
+      if (__any_sync(0xffffffffu, frag)) O += 1.f;  // stand-in for the exact step
+    }
+    if (V >= 2) {
 #pragma unroll
       for (int p = 0; p < K; ++p) { vb[p] = nvb[p]; vl[p] = nvl[p]; }
       O += shp;
@@ -112,6 +132,8 @@ int main() {
   run<2, 0>(out, cyc); run<3, 0>(out, cyc); run<4, 0>(out, cyc); run<5, 0>(out, cyc); run<6, 0>(out, cyc);
   run<2, 1>(out, cyc); run<3, 1>(out, cyc); run<4, 1>(out, cyc); run<5, 1>(out, cyc); run<6, 1>(out, cyc);
   run<2, 2>(out, cyc); run<3, 2>(out, cyc); run<4, 2>(out, cyc); run<5, 2>(out, cyc); run<6, 2>(out, cyc);
+  run<2, 3>(out, cyc); run<3, 3>(out, cyc); run<4, 3>(out, cyc); run<5, 3>(out, cyc); run<6, 3>(out, cyc);
+  run<2, 4>(out, cyc); run<3, 4>(out, cyc); run<4, 4>(out, cyc); run<5, 4>(out, cyc); run<6, 4>(out, cyc);
   printf("status %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
 }
