@@ -39,6 +39,26 @@ def _newer(target: str, deps) -> bool:
     return all(os.path.getmtime(d) <= t for d in deps)
 
 
+def check_no_stack(src: str, ptxas_log: str) -> None:
+    """Refuses kernels that need a local-memory stack frame (register spills).
+
+    ptxas 12.9 for sm_100a was seen to reuse R1 -- the stack pointer -- as a
+    general register in the spilling k_pair<8> instantiation, so its STL/LDL
+    hit wild local addresses (an illegal-address fault only for some label
+    lengths). The kernels are written to fit in registers; a build that spills
+    fails here instead of shipping."""
+    cur = None
+    for line in ptxas_log.splitlines():
+        if "Function properties for" in line:
+            cur = line.split("Function properties for")[-1].strip()
+        elif cur and "bytes stack frame" in line:
+            frame = int(line.strip().split()[0])
+            if frame and "watchdog" not in cur:
+                raise RuntimeError(f"{src}: {cur} needs a {frame}-byte stack frame (register spill); "
+                                   "refusing the build (see build.check_no_stack)")
+            cur = None
+
+
 def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB, build_dir: str = BUILD) -> str:
     """Builds the library. `defines` (debug experiments only, e.g. ("DS2CTC_EXP_NOOCC",))
     go to a separate `lib` / `build_dir`; the product library is built without any."""
@@ -60,6 +80,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB
             raise RuntimeError(f"nvcc failed:\n{' '.join(cmd)}\n{res.stderr}")
         with open(os.path.join(BUILD_, src + ".ptxas.txt"), "w") as f:
             f.write(res.stderr)
+        check_no_stack(src, res.stderr)
         if verbose:
             print(res.stderr)
         objs.append(obj)

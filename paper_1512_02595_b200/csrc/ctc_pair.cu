@@ -87,6 +87,7 @@ __device__ __forceinline__ float lse3f(float a, float b, float c) {
 }
 
 __device__ __forceinline__ void cluster_barrier() {
+  __syncwarp();  // .aligned: the whole warp must arrive converged
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
@@ -317,7 +318,6 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   float* emis = reinterpret_cast<float*>(smem + g.off_emis);
   float2* lser = reinterpret_cast<float2*>(smem + g.off_lse);
   float* el = reinterpret_cast<float*>(smem + g.off_el);
-  float* tile = reinterpret_cast<float*>(smem + g.off_tile);
   float* occs = reinterpret_cast<float*>(smem + g.off_occ);
   unsigned long long* ring = reinterpret_cast<unsigned long long*>(smem + g.off_ring);
   int* s_lab = reinterpret_cast<int*>(smem + g.off_meta);
@@ -478,15 +478,18 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     }
     __syncwarp();
   };
-  // Gradient rows of a finished phase-2 epoch, lane = row (ctc.cpp:196-203,
-  // 69-79). All lanes walk the same (uniform) index sequences, so every loop
-  // is divergence-free and the 32 rows proceed in lock step.
-  auto grad_rows = [&](const Epoch& e) {
+  // Gradient rows of a finished phase-2 epoch (ctc.cpp:196-203, 69-79) in two
+  // stages on two warps: grad_occ (gradient warp, one epoch behind the
+  // chain) sums the label occupancies per key slot into occs[half];
+  // grad_write (service warp, one epoch later) forms softmax - occupancy and
+  // stores the rows. Lane = row; all lanes walk the same (uniform) index
+  // sequences, so every loop is divergence-free.
+  auto grad_occ = [&](const Epoch& e, int half) {
     if (e.phase != 2) return;
     const int n = e.k1 - e.k0;
     const int k = e.k0 + (lane < n ? lane : 0);
     const float* elr = el + (k & M2) * g.estride;
-    float* oc = occs + lane * g.ostride;
+    float* oc = occs + (half * 32 + lane) * g.ostride;
     // Label cells in one flat pass over the slot-sorted positions of slots
     // >= 1 (every one of them has positions), flushing at slot changes. The
     // blank slot is the rest of the frame's unit mass: sum_s gamma(s, t) = 1
@@ -520,35 +523,32 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
       tot += acc;
     }
     oc[0] = 1.f - tot;
-    float* tr = tile + lane * g.tstride;
-    if (fused) {
-      const float2 st = lser[k & MX];
-      const float* xr = xraw + (k & MX) * g.xstride;
-#pragma unroll 4
-      for (int c = 0; c < a.A; ++c) {
-        const int slot = s_slot[c];
-        const float soft = ex2(((xr[c] - st.x) - st.y) * kL2eH);
-        tr[c] = soft - (slot >= 0 ? oc[slot] : 0.f);
-      }
-    } else {
-      for (int j = 0; j < u.nkey; ++j) tr[j] = oc[j];
-    }
-    __syncwarp();
-    // one row per iteration, lane = symbol: coalesced row stores
+  };
+  auto grad_write = [&](const Epoch& e, int half) {
+    if (e.phase != 2) return;
+    const int n = e.k1 - e.k0;
+    // one row per iteration, lane = symbol: reads conflict-free, stores coalesced
     if (fused) {
       float* gb = a.grad + static_cast<size_t>(b) * a.A;
       for (int c = lane; c < a.A; c += 32) {
-#pragma unroll 4
-        for (int r = 0; r < n; ++r) gb[static_cast<size_t>(frame(e.k0 + r)) * rs + c] = tile[r * g.tstride + c];
+        const int slot = s_slot[c];
+#pragma unroll 2
+        for (int r = 0; r < n; ++r) {
+          const int k = e.k0 + r;
+          const float2 st = lser[k & MX];
+          const float* oc = occs + (half * 32 + r) * g.ostride;
+          const float soft = ex2(((xraw[(k & MX) * g.xstride + c] - st.x) - st.y) * kL2eH);
+          gb[static_cast<size_t>(frame(k)) * rs + c] = soft - (slot >= 0 ? oc[slot] : 0.f);
+        }
       }
     } else {
       float* ob = a.occ + u.occ_off;
-      for (int c = lane; c < u.nkey; c += 32) {
+      for (int j = lane; j < u.nkey; j += 32) {
 #pragma unroll 4
-        for (int r = 0; r < n; ++r) ob[static_cast<size_t>(frame(e.k0 + r)) * u.nkey + c] = tile[r * g.tstride + c];
+        for (int r = 0; r < n; ++r)
+          ob[static_cast<size_t>(frame(e.k0 + r)) * u.nkey + j] = occs[(half * 32 + r) * g.ostride + j];
       }
     }
-    __syncwarp();
   };
 
   // =====================================================================
@@ -887,7 +887,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   }
   __syncthreads();
 
-  Epoch prev{0, 0, 0};
+  Epoch prev{0, 0, 0}, prev2{0, 0, 0};
   bool dead = false;
 #ifdef DS2CTC_EPOCH_TIMING
   int epoch_idx = 0;
@@ -926,12 +926,18 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
 #ifdef DS2CTC_EPOCH_TIMING
       if (stamp) g_step_clock[dir][7][epoch_idx][3] = clock64();
 #endif
+#ifndef DS2CTC_EXP_NOGRAD
+      grad_write(prev2, (ep - 2) & 1);
+#endif
+#ifdef DS2CTC_EPOCH_TIMING
+      if (stamp) g_step_clock[dir][6][epoch_idx][0] = clock64();
+#endif
 #endif
       // the previous epoch's half must be read out before the next epoch refills it
       if (lane == 0 && cur.phase == 1) bulk_wait_read0();
     } else if (grad_warp) {
 #ifndef DS2CTC_EXP_NOGRAD
-      grad_rows(prev);
+      grad_occ(prev, (ep - 1) & 1);
 #endif
     } else if (is_chain) {
       chain_epoch(cur);
@@ -1024,12 +1030,21 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
       __syncthreads();
       MEET_STAMP(5);
     }
+    prev2 = prev;
     prev = cur;
     cur = nxt;
     ++ep;
   }
   MEET_STAMP(7);
-  if (grad_warp && !dead && want_grad) grad_rows(prev);  // the last phase-2 epoch
+  // drain: the last two epochs' gradient rows (grad_occ runs one epoch behind
+  // the chain, grad_write two); CTA-uniform condition
+  if (!dead && want_grad) {
+    if (grad_warp) grad_occ(prev, (ep - 1) & 1);
+    if (service) grad_write(prev2, (ep - 2) & 1);
+    __syncthreads();
+    if (service) grad_write(prev, (ep - 1) & 1);
+    __syncthreads();
+  }
 
   // ---- costs: fused cost = sum_t ls_t - log Z' (natural log; log Z' of the shifted frames) ----
   if (service) {

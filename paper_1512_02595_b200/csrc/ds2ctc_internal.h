@@ -62,7 +62,7 @@ struct Geometry {
   int max_L;
   int fused;
   // shared-memory carve-up (bytes, 16-aligned)
-  int off_xraw, off_emis, off_lse, off_el, off_tile, off_occ, off_ring, off_meta, off_red;
+  int off_xraw, off_emis, off_lse, off_el, off_occ, off_ring, off_meta, off_red;
   int ring_depth; // halo refresh ring entries per chain warp
   int off_cb;     // column buffer [2][P][cw_max] floats (TMA bulk stores / loads of lattice columns)
   int off_mbar;   // two mbarriers (one per column-buffer half)
@@ -70,7 +70,6 @@ struct Geometry {
   int xstride;    // floats per xraw row (odd)
   int estride;    // floats per eb/el row (odd)
   int cw_max;     // floats per stored column (max over batch)
-  int tstride;    // floats per tile row (odd)
   int ostride;    // floats per occ scratch row (odd)
   int smem;       // total bytes
 };
@@ -117,7 +116,6 @@ inline Geometry make_geometry(int max_L_all, int max_L, int max_nkey, int A, boo
     g.P = P;
     g.xstride = g.SW | 1;
     g.estride = (max_L + 1) | 1;
-    g.tstride = (fused ? A : max_nkey) | 1;
     g.ostride = max_nkey | 1;
     int off = 0;
     auto take = [&](int bytes) {
@@ -130,8 +128,7 @@ inline Geometry make_geometry(int max_L_all, int max_L, int max_nkey, int A, boo
     g.off_emis = take(4 * 2 * P * emis_stride(g.SW));  // + a sentinel column for cells that do not exist
     g.off_lse = take(8 * RX);
     g.off_el = take(4 * 2 * P * g.estride);
-    g.off_tile = take(4 * 32 * g.tstride);  // one row per service lane (all 32 lanes run, P <= 32)
-    g.off_occ = take(4 * 32 * g.ostride);
+    g.off_occ = take(4 * 2 * 32 * g.ostride);  // double-buffered: label sums of epoch e-1 || gradient rows of e-2
     g.ring_depth = 4;  // a power of two >= 2 * (P / halo_steps + 2): the slot is a mask, not a division
     while (g.ring_depth < 2 * (P / halo_steps(g.K) + 2)) g.ring_depth *= 2;
     g.off_ring = take(8 * g.nchain * g.ring_depth * kHaloLanes * (2 * g.K + 1));

@@ -90,7 +90,8 @@ def run(so, A=29, T=700, L=150, B=64, brief=False):
             sv = steps[cta, 7]
             for ep in (2, len(rows) - 3):
                 if 0 < ep < 32 and sv[ep, 0] > 0:
-                    print(f"  cta{cta}: service epoch {ep}: stage+grad_rows {sv[ep,1]-sv[ep,0]}, wait {sv[ep,2]-sv[ep,1]}, convert {sv[ep,3]-sv[ep,2]}")
+                    print(f"  cta{cta}: service epoch {ep}: stage {sv[ep,1]-sv[ep,0]}, wait {sv[ep,2]-sv[ep,1]}, "
+                          f"convert {sv[ep,3]-sv[ep,2]}, grad_write {steps[cta, 6, ep, 0] - sv[ep,3]}")
             busy = np.mean([[int(r[w, 1] - r[w, 0]) for w in range(8)] for r in p1], axis=0)
             # service = warp 0, chain warps 1..NCW; per-step cycles over the stamped phase-2 epoch
             for w in (1, 2, 3):
