@@ -107,6 +107,30 @@ ds2ctc_status ds2ctc_compute_loss_host(const float* activations, float* gradient
                                        int minibatch, int blank_label, float* costs, int device);
 
 /*
+ * CTC forced alignment, the batched device counterpart of
+ *   std::vector<int> viterbi_align(const Matrix& frame_logprobs,
+ *                                  const std::vector<int>& label, int blank)
+ * (proj/include/asr/ctc.hpp:97-101, proj/src/ctc.cpp:327-370), used by
+ * datapipe::align_frames / segment (datapipe.cpp:27-92) and `asr align`.
+ * For each b: the highest-probability lattice path of X[0:T_b, b, :] whose
+ * collapse is the label, ties resolved exactly as the reference (stay >
+ * advance > skip; terminal blank unless the terminal label is strictly
+ * better). alignments is DEVICE int32 [minibatch][T_max] (T_max = max T_b):
+ * the frame symbols, -1 past T_b. status is DEVICE int32 [minibatch]: 0 =
+ * aligned, 1 = no alignment (T_b < min_frames, T_b == 0, or every path has
+ * zero probability -- where the reference throws; the row is all -1).
+ * activations as ds2ctc_compute_loss; labels and lengths are host arrays.
+ * Asynchronous on `stream`; the workspace comes from
+ * ds2ctc_viterbi_get_workspace_size (per-utterance backpointers).
+ */
+ds2ctc_status ds2ctc_viterbi_get_workspace_size(const int* label_lengths, const int* input_lengths,
+                                                int alphabet_size, int minibatch, size_t* bytes);
+ds2ctc_status ds2ctc_viterbi_align(const float* activations, const int* flat_labels, const int* label_lengths,
+                                   const int* input_lengths, int alphabet_size, int minibatch, int blank_label,
+                                   int* alignments, int* status, void* workspace, size_t workspace_bytes,
+                                   void* stream);
+
+/*
  * Per-shard {sum of feasible costs, number of infeasible utterances} as fp64
  * [2] on the device, the two scalars train_epoch accumulates
  * (local_loss / local_skipped, trainer.cpp:160-168) and all-reduces

@@ -296,6 +296,62 @@ ds2ctc_status run(const float* acts, float* grads, const int* flat_labels, const
   return DS2CTC_STATUS_SUCCESS;
 }
 
+ds2ctc_status run_viterbi(const float* acts, const int* flat_labels, const int* label_lengths,
+                          const int* input_lengths, int A, int B, int blank, int* alignments, int* status,
+                          void* workspace, size_t workspace_bytes, void* stream) {
+  ds2ctc_status st = validate(label_lengths, input_lengths, A, B, blank, flat_labels);
+  if (st != DS2CTC_STATUS_SUCCESS) return st;
+  if (B == 0) return DS2CTC_STATUS_SUCCESS;
+  const ViterbiLayout lay = make_viterbi_layout(label_lengths, input_lengths, B);
+  if (alignments == nullptr || status == nullptr || workspace == nullptr) return DS2CTC_STATUS_INVALID_VALUE;
+  if (lay.t_max > 0 && acts == nullptr) return DS2CTC_STATUS_INVALID_VALUE;
+  if (workspace_bytes < lay.total) return DS2CTC_STATUS_INVALID_VALUE;
+  if (reinterpret_cast<uintptr_t>(workspace) % kAlign != 0) return DS2CTC_STATUS_INVALID_VALUE;
+  // host blob: descriptors + labels (min_frames pre-check as ctc.cpp:328)
+  const size_t meta = lay.bp;
+  thread_local std::vector<unsigned char> blob;
+  blob.assign(meta, 0);
+  auto* desc = reinterpret_cast<ViterbiDesc*>(blob.data() + lay.desc);
+  long long lab_off = 0, bp_off = 0;
+  size_t smem = 0;
+  for (int b = 0; b < B; ++b) {
+    const int T = input_lengths[b], L = label_lengths[b];
+    ViterbiDesc& d = desc[b];
+    d.T = T;
+    d.L = L;
+    d.lab_off = static_cast<int>(lab_off);
+    d.status = (T == 0 || T < min_frames(flat_labels + lab_off, L)) ? 1 : 0;
+    d.bp_off = bp_off;
+    d.pad = 0;
+    if (d.status == 0) smem = std::max(smem, viterbi_smem_bytes(T, L));
+    lab_off += L;
+    bp_off += static_cast<long long>(T) * (2LL * L + 1);
+  }
+  if (lab_off > 0) std::memcpy(blob.data() + lay.labels, flat_labels, sizeof(int) * lab_off);
+  if (smem > kSmemBudget) return DS2CTC_STATUS_UNSUPPORTED;
+  auto* ws = static_cast<unsigned char*>(workspace);
+  auto s = static_cast<cudaStream_t>(stream);
+  cudaEvent_t ev = nullptr;
+  void* pinned = staging_for_current_device().acquire(meta, &ev);
+  if (pinned == nullptr) return DS2CTC_STATUS_MEMOPS_FAILED;
+  std::memcpy(pinned, blob.data(), meta);
+  if (cudaMemcpyAsync(ws, pinned, meta, cudaMemcpyHostToDevice, s) != cudaSuccess) return DS2CTC_STATUS_MEMOPS_FAILED;
+  if (cudaEventRecord(ev, s) != cudaSuccess) return DS2CTC_STATUS_MEMOPS_FAILED;
+  ViterbiArgs a{};
+  a.x = acts;
+  a.desc = reinterpret_cast<const ViterbiDesc*>(ws + lay.desc);
+  a.labels = reinterpret_cast<const int*>(ws + lay.labels);
+  a.bp = ws + lay.bp;
+  a.align = alignments;
+  a.status = status;
+  a.t_max = lay.t_max;
+  a.B = B;
+  a.A = A;
+  a.blank = blank;
+  if (launch_viterbi(a, smem, stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  return DS2CTC_STATUS_SUCCESS;
+}
+
 // Per-thread device context of the host-buffer entry point.
 struct HostContext {
   int device = -1;
@@ -375,6 +431,24 @@ ds2ctc_status ds2ctc_compute_loss_checked(const float* activations, float* gradi
                                           size_t workspace_bytes, void* stream) {
   return run(activations, gradients, flat_labels, label_lengths, input_lengths, alphabet_size, minibatch,
              blank_label, costs, workspace, workspace_bytes, true, stream);
+}
+
+ds2ctc_status ds2ctc_viterbi_get_workspace_size(const int* label_lengths, const int* input_lengths,
+                                                int alphabet_size, int minibatch, size_t* bytes) {
+  if (bytes == nullptr || minibatch < 0 || alphabet_size < 2) return DS2CTC_STATUS_INVALID_VALUE;
+  if (minibatch > 0 && (label_lengths == nullptr || input_lengths == nullptr)) return DS2CTC_STATUS_INVALID_VALUE;
+  for (int b = 0; b < minibatch; ++b)
+    if (label_lengths[b] < 0 || input_lengths[b] < 0) return DS2CTC_STATUS_INVALID_VALUE;
+  *bytes = make_viterbi_layout(label_lengths, input_lengths, minibatch).total;
+  return DS2CTC_STATUS_SUCCESS;
+}
+
+ds2ctc_status ds2ctc_viterbi_align(const float* activations, const int* flat_labels, const int* label_lengths,
+                                   const int* input_lengths, int alphabet_size, int minibatch, int blank_label,
+                                   int* alignments, int* status, void* workspace, size_t workspace_bytes,
+                                   void* stream) {
+  return run_viterbi(activations, flat_labels, label_lengths, input_lengths, alphabet_size, minibatch, blank_label,
+                     alignments, status, workspace, workspace_bytes, stream);
 }
 
 ds2ctc_status ds2ctc_loss_sum(const float* costs, int minibatch, double* out2, void* stream) {

@@ -214,11 +214,56 @@ struct PairArgs {
   Geometry g;
 };
 
-// Launchers (ctc_pair.cu / ctc_dense.cu). Return cudaError_t as int.
+// Forced alignment (ctc_viterbi.cu; viterbi_align, ctc.cpp:327-370).
+struct alignas(16) ViterbiDesc {
+  int T, L, lab_off, status;  // status 1: T < min_frames or T == 0 (the reference throws)
+  long long bp_off;           // byte offset of the utterance's [T][2L+1] backpointers
+  long long pad;
+};
+static_assert(sizeof(ViterbiDesc) == 32, "ViterbiDesc layout");
+
+struct ViterbiArgs {
+  const float* x;  // [T_max][B][A]
+  const ViterbiDesc* desc;
+  const int* labels;
+  unsigned char* bp;
+  int* align;   // [B][T_max]: alignment symbols, -1 past T_b or without alignment
+  int* status;  // [B]: 0 aligned, 1 infeasible / no path of nonzero probability
+  int t_max, B, A, blank;
+};
+
+struct ViterbiLayout {
+  size_t desc, labels, bp, total;
+  int t_max;
+};
+
+inline ViterbiLayout make_viterbi_layout(const int* label_lengths, const int* input_lengths, int B) {
+  ViterbiLayout v{};
+  long long sum_L = 0, bp = 0;
+  for (int b = 0; b < B; ++b) {
+    sum_L += label_lengths[b];
+    bp += static_cast<long long>(input_lengths[b]) * (2LL * label_lengths[b] + 1);
+    v.t_max = input_lengths[b] > v.t_max ? input_lengths[b] : v.t_max;
+  }
+  size_t off = 0;
+  v.desc = off;
+  off += sizeof(ViterbiDesc) * B;
+  v.labels = off;
+  off += sizeof(int) * static_cast<size_t>(sum_L);
+  off = (off + kAlign - 1) / kAlign * kAlign;
+  v.bp = off;
+  off += static_cast<size_t>(bp);
+  v.total = B > 0 ? (off + kAlign - 1) / kAlign * kAlign : 0;
+  return v;
+}
+
+// Launchers (ctc_pair.cu / ctc_dense.cu / ctc_viterbi.cu). Return cudaError_t as int.
 int launch_pair(const PairArgs& a, void* stream);
 int launch_dense(const PairArgs& a, bool write_grad, void* stream);
 int launch_finalize(const PairArgs& a, void* stream);
 int launch_loss_sum(const float* costs, int B, double* out2, void* stream);
 int read_watchdog(unsigned long long* out4);
+size_t viterbi_smem_bytes(int T, int L);
+int launch_viterbi(const ViterbiArgs& a, size_t smem, void* stream);
 
 }  // namespace ds2ctc

@@ -150,3 +150,60 @@ def ctc_loss(frame_logits, label: Sequence[int], blank: int, device: int = 0) ->
     if not np.isfinite(loss):
         return CtcResult(False, float("inf"), np.zeros((0, 0), dtype=np.float32))
     return CtcResult(True, loss, grads.reshape(T, A))
+
+
+def viterbi_workspace_size(label_lengths, input_lengths, alphabet_size: int) -> int:
+    """ds2ctc_viterbi_get_workspace_size: device bytes for one alignment call."""
+    ll = _i32(label_lengths)
+    il = _i32(input_lengths)
+    B = int(np.asarray(label_lengths).size)
+    out = ctypes.c_size_t()
+    _lib.check(_lib.lib().ds2ctc_viterbi_get_workspace_size(_iptr(ll), _iptr(il), alphabet_size, B,
+                                                            ctypes.byref(out)),
+               "ds2ctc_viterbi_get_workspace_size")
+    return int(out.value)
+
+
+def viterbi_align_batch(activations, flat_labels, label_lengths, input_lengths, blank: Optional[int] = None,
+                        workspace: Optional[Workspace] = None, stream=None):
+    """Batched forced alignment on the GPU (ds2ctc_viterbi_align).
+
+    activations: contiguous float32 CUDA tensor [T_max, B, A]. Returns
+    (alignments int32 CUDA [B, T_max] with -1 past T_b, status int32 CUDA [B]:
+    0 aligned, 1 no alignment -- where the reference throws)."""
+    import torch
+
+    if not (activations.is_cuda and activations.dtype == torch.float32 and activations.is_contiguous()):
+        raise ValueError("activations must be a contiguous float32 CUDA tensor [T, B, A]")
+    T_max, B, A = activations.shape
+    blank = A - 1 if blank is None else int(blank)
+    dev = activations.device
+    align = torch.empty((max(B, 1), max(T_max, 1)), dtype=torch.int32, device=dev)
+    status = torch.empty(max(B, 1), dtype=torch.int32, device=dev)
+    if workspace is None:
+        workspace = _default_ws.setdefault(dev.index, Workspace(dev))
+    ws_ptr, ws_bytes = workspace.get(viterbi_workspace_size(label_lengths, input_lengths, A))
+    if stream is None:
+        stream = torch.cuda.current_stream(dev)
+    st = _lib.lib().ds2ctc_viterbi_align(
+        ctypes.c_void_p(activations.data_ptr()), _iptr(_i32(flat_labels)), _iptr(_i32(label_lengths)),
+        _iptr(_i32(input_lengths)), A, B, blank, ctypes.c_void_p(align.data_ptr()),
+        ctypes.c_void_p(status.data_ptr()), ctypes.c_void_p(ws_ptr), ws_bytes, ctypes.c_void_p(stream.cuda_stream))
+    _lib.check(st, "ds2ctc_viterbi_align")
+    return align[:B, :T_max], status[:B]
+
+
+def viterbi_align(frame_logits, label: Sequence[int], blank: int, device: int = 0):
+    """Drop-in for asr::ctc::viterbi_align (ctc.cpp:327-370) on one utterance:
+    the frame symbols of the best alignment; raises ValueError where the
+    reference throws (label infeasible for T, or no path of nonzero probability)."""
+    import torch
+
+    x = np.ascontiguousarray(np.asarray(frame_logits, dtype=np.float32))
+    T, A = x.shape
+    lab = [int(c) for c in label]
+    xt = torch.from_numpy(x.reshape(T, 1, A)).to(torch.device("cuda", device))
+    align, status = viterbi_align_batch(xt, lab, [len(lab)], [T], blank=blank)
+    if int(status[0].item()) != 0:
+        raise ValueError("viterbi_align: label infeasible for frame count or no feasible path")
+    return align[0].cpu().numpy().astype(np.int64).tolist()
