@@ -131,6 +131,27 @@ ds2ctc_status ds2ctc_viterbi_align(const float* activations, const int* flat_lab
                                    void* stream);
 
 /*
+ * Full CTC lattice export, the batched device counterpart
+ * of CtcLattice ctc_lattice(const Matrix& frame_logits, const std::vector<int>&
+ * label, int blank) (proj/include/asr/ctc.hpp:55-60,68-71; ctc.cpp:145-169):
+ * fp64 natural-log alpha and emission-exclusive beta of every lattice cell
+ * and log p, computed operation by operation as the reference (debug /
+ * verification path of the column-parallel scheme). ds2ctc_lattice_get_sizes
+ * gives the cell count (sum_b (2 L_b + 1) T_b) of alpha and of beta, and the
+ * workspace bytes. alpha / beta are DEVICE fp64 [cells]: utterance b's block
+ * starts at sum_{b'<b} (2 L_b' + 1) T_b' and is row-major [2 L_b + 1][T_b]
+ * (the reference Matrix (s, t)); log_prob is DEVICE fp64 [minibatch] (-inf
+ * when no path has nonzero probability). Every T_b must be >= 1 (the
+ * reference throws, ctc.cpp:146): INVALID_VALUE otherwise.
+ */
+ds2ctc_status ds2ctc_lattice_get_sizes(const int* label_lengths, const int* input_lengths, int minibatch,
+                                       size_t* cells, size_t* workspace_bytes);
+ds2ctc_status ds2ctc_ctc_lattice(const float* activations, const int* flat_labels, const int* label_lengths,
+                                 const int* input_lengths, int alphabet_size, int minibatch, int blank_label,
+                                 double* alpha, double* beta, double* log_prob, void* workspace,
+                                 size_t workspace_bytes, void* stream);
+
+/*
  * Per-shard {sum of feasible costs, number of infeasible utterances} as fp64
  * [2] on the device, the two scalars train_epoch accumulates
  * (local_loss / local_skipped, trainer.cpp:160-168) and all-reduces

@@ -33,6 +33,8 @@ EXPORTS = (
     "ds2ctc_loss_sum",
     "ds2ctc_viterbi_get_workspace_size",
     "ds2ctc_viterbi_align",
+    "ds2ctc_lattice_get_sizes",
+    "ds2ctc_ctc_lattice",
     "ds2ctc_profile_enable",
     "ds2ctc_profile_read",
     "ds2ctc_debug_watchdog",
@@ -88,6 +90,11 @@ def lib():
             L.ds2ctc_loss_sum.argtypes = [_p, ctypes.c_int, _p, _p]
             L.ds2ctc_viterbi_get_workspace_size.restype = ctypes.c_int
             L.ds2ctc_viterbi_get_workspace_size.argtypes = [_ip, _ip, ctypes.c_int, ctypes.c_int, _szp]
+            L.ds2ctc_lattice_get_sizes.restype = ctypes.c_int
+            L.ds2ctc_lattice_get_sizes.argtypes = [_ip, _ip, ctypes.c_int, _szp, _szp]
+            L.ds2ctc_ctc_lattice.restype = ctypes.c_int
+            L.ds2ctc_ctc_lattice.argtypes = [_p, _ip, _ip, _ip, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p, _p, _p,
+                                             _p, ctypes.c_size_t, _p]
             L.ds2ctc_viterbi_align.restype = ctypes.c_int
             L.ds2ctc_viterbi_align.argtypes = [_p, _ip, _ip, _ip, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p, _p,
                                                _p, ctypes.c_size_t, _p]

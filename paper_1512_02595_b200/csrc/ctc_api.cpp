@@ -296,6 +296,75 @@ ds2ctc_status run(const float* acts, float* grads, const int* flat_labels, const
   return DS2CTC_STATUS_SUCCESS;
 }
 
+// Descriptors + labels of the fp64 lattice paths (alignment, export) into
+// the workspace head; returns the largest per-CTA shared-memory need.
+ds2ctc_status stage_lattice_meta(const ViterbiLayout& lay, const int* flat_labels, const int* label_lengths,
+                                 const int* input_lengths, int B, void* workspace, void* stream, size_t* smem_out) {
+  const size_t meta = lay.bp;
+  thread_local std::vector<unsigned char> blob;
+  blob.assign(meta, 0);
+  auto* desc = reinterpret_cast<ViterbiDesc*>(blob.data() + lay.desc);
+  long long lab_off = 0, cell_off = 0;
+  size_t smem = 0;
+  for (int b = 0; b < B; ++b) {
+    const int T = input_lengths[b], L = label_lengths[b];
+    ViterbiDesc& d = desc[b];
+    d.T = T;
+    d.L = L;
+    d.lab_off = static_cast<int>(lab_off);
+    d.status = (T == 0 || T < min_frames(flat_labels + lab_off, L)) ? 1 : 0;  // ctc.cpp:328
+    d.bp_off = cell_off;
+    d.pad = 0;
+    smem = std::max(smem, viterbi_smem_bytes(T, L));  // == lattice_smem_bytes
+    lab_off += L;
+    cell_off += static_cast<long long>(T) * (2LL * L + 1);
+  }
+  if (lab_off > 0) std::memcpy(blob.data() + lay.labels, flat_labels, sizeof(int) * lab_off);
+  if (smem > kSmemBudget) return DS2CTC_STATUS_UNSUPPORTED;
+  auto s = static_cast<cudaStream_t>(stream);
+  cudaEvent_t ev = nullptr;
+  void* pinned = staging_for_current_device().acquire(meta, &ev);
+  if (pinned == nullptr) return DS2CTC_STATUS_MEMOPS_FAILED;
+  std::memcpy(pinned, blob.data(), meta);
+  if (cudaMemcpyAsync(workspace, pinned, meta, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return DS2CTC_STATUS_MEMOPS_FAILED;
+  if (cudaEventRecord(ev, s) != cudaSuccess) return DS2CTC_STATUS_MEMOPS_FAILED;
+  *smem_out = smem;
+  return DS2CTC_STATUS_SUCCESS;
+}
+
+ds2ctc_status run_lattice(const float* acts, const int* flat_labels, const int* label_lengths,
+                          const int* input_lengths, int A, int B, int blank, double* alpha, double* beta,
+                          double* log_prob, void* workspace, size_t workspace_bytes, void* stream) {
+  ds2ctc_status st = validate(label_lengths, input_lengths, A, B, blank, flat_labels);
+  if (st != DS2CTC_STATUS_SUCCESS) return st;
+  for (int b = 0; b < B; ++b)
+    if (input_lengths[b] < 1) return DS2CTC_STATUS_INVALID_VALUE;  // ctc_lattice requires T >= 1 (ctc.cpp:146)
+  if (B == 0) return DS2CTC_STATUS_SUCCESS;
+  const ViterbiLayout lay = make_viterbi_layout(label_lengths, input_lengths, B);
+  if (acts == nullptr || alpha == nullptr || beta == nullptr || log_prob == nullptr || workspace == nullptr)
+    return DS2CTC_STATUS_INVALID_VALUE;
+  if (workspace_bytes < lay.bp || reinterpret_cast<uintptr_t>(workspace) % kAlign != 0)
+    return DS2CTC_STATUS_INVALID_VALUE;
+  size_t smem = 0;
+  st = stage_lattice_meta(lay, flat_labels, label_lengths, input_lengths, B, workspace, stream, &smem);
+  if (st != DS2CTC_STATUS_SUCCESS) return st;
+  auto* ws = static_cast<unsigned char*>(workspace);
+  LatticeArgs a{};
+  a.x = acts;
+  a.desc = reinterpret_cast<const ViterbiDesc*>(ws + lay.desc);
+  a.labels = reinterpret_cast<const int*>(ws + lay.labels);
+  a.alpha = alpha;
+  a.beta = beta;
+  a.log_prob = log_prob;
+  a.t_max = lay.t_max;
+  a.B = B;
+  a.A = A;
+  a.blank = blank;
+  if (launch_lattice(a, smem, stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  return DS2CTC_STATUS_SUCCESS;
+}
+
 ds2ctc_status run_viterbi(const float* acts, const int* flat_labels, const int* label_lengths,
                           const int* input_lengths, int A, int B, int blank, int* alignments, int* status,
                           void* workspace, size_t workspace_bytes, void* stream) {
@@ -307,36 +376,10 @@ ds2ctc_status run_viterbi(const float* acts, const int* flat_labels, const int* 
   if (lay.t_max > 0 && acts == nullptr) return DS2CTC_STATUS_INVALID_VALUE;
   if (workspace_bytes < lay.total) return DS2CTC_STATUS_INVALID_VALUE;
   if (reinterpret_cast<uintptr_t>(workspace) % kAlign != 0) return DS2CTC_STATUS_INVALID_VALUE;
-  // host blob: descriptors + labels (min_frames pre-check as ctc.cpp:328)
-  const size_t meta = lay.bp;
-  thread_local std::vector<unsigned char> blob;
-  blob.assign(meta, 0);
-  auto* desc = reinterpret_cast<ViterbiDesc*>(blob.data() + lay.desc);
-  long long lab_off = 0, bp_off = 0;
   size_t smem = 0;
-  for (int b = 0; b < B; ++b) {
-    const int T = input_lengths[b], L = label_lengths[b];
-    ViterbiDesc& d = desc[b];
-    d.T = T;
-    d.L = L;
-    d.lab_off = static_cast<int>(lab_off);
-    d.status = (T == 0 || T < min_frames(flat_labels + lab_off, L)) ? 1 : 0;
-    d.bp_off = bp_off;
-    d.pad = 0;
-    if (d.status == 0) smem = std::max(smem, viterbi_smem_bytes(T, L));
-    lab_off += L;
-    bp_off += static_cast<long long>(T) * (2LL * L + 1);
-  }
-  if (lab_off > 0) std::memcpy(blob.data() + lay.labels, flat_labels, sizeof(int) * lab_off);
-  if (smem > kSmemBudget) return DS2CTC_STATUS_UNSUPPORTED;
+  st = stage_lattice_meta(lay, flat_labels, label_lengths, input_lengths, B, workspace, stream, &smem);
+  if (st != DS2CTC_STATUS_SUCCESS) return st;
   auto* ws = static_cast<unsigned char*>(workspace);
-  auto s = static_cast<cudaStream_t>(stream);
-  cudaEvent_t ev = nullptr;
-  void* pinned = staging_for_current_device().acquire(meta, &ev);
-  if (pinned == nullptr) return DS2CTC_STATUS_MEMOPS_FAILED;
-  std::memcpy(pinned, blob.data(), meta);
-  if (cudaMemcpyAsync(ws, pinned, meta, cudaMemcpyHostToDevice, s) != cudaSuccess) return DS2CTC_STATUS_MEMOPS_FAILED;
-  if (cudaEventRecord(ev, s) != cudaSuccess) return DS2CTC_STATUS_MEMOPS_FAILED;
   ViterbiArgs a{};
   a.x = acts;
   a.desc = reinterpret_cast<const ViterbiDesc*>(ws + lay.desc);
@@ -449,6 +492,28 @@ ds2ctc_status ds2ctc_viterbi_align(const float* activations, const int* flat_lab
                                    void* stream) {
   return run_viterbi(activations, flat_labels, label_lengths, input_lengths, alphabet_size, minibatch, blank_label,
                      alignments, status, workspace, workspace_bytes, stream);
+}
+
+ds2ctc_status ds2ctc_lattice_get_sizes(const int* label_lengths, const int* input_lengths, int minibatch,
+                                       size_t* cells, size_t* workspace_bytes) {
+  if (cells == nullptr || workspace_bytes == nullptr || minibatch < 0) return DS2CTC_STATUS_INVALID_VALUE;
+  if (minibatch > 0 && (label_lengths == nullptr || input_lengths == nullptr)) return DS2CTC_STATUS_INVALID_VALUE;
+  size_t n = 0;
+  for (int b = 0; b < minibatch; ++b) {
+    if (label_lengths[b] < 0 || input_lengths[b] < 0) return DS2CTC_STATUS_INVALID_VALUE;
+    n += static_cast<size_t>(input_lengths[b]) * (2 * static_cast<size_t>(label_lengths[b]) + 1);
+  }
+  *cells = n;
+  *workspace_bytes = make_viterbi_layout(label_lengths, input_lengths, minibatch).bp;  // metadata only
+  return DS2CTC_STATUS_SUCCESS;
+}
+
+ds2ctc_status ds2ctc_ctc_lattice(const float* activations, const int* flat_labels, const int* label_lengths,
+                                 const int* input_lengths, int alphabet_size, int minibatch, int blank_label,
+                                 double* alpha, double* beta, double* log_prob, void* workspace,
+                                 size_t workspace_bytes, void* stream) {
+  return run_lattice(activations, flat_labels, label_lengths, input_lengths, alphabet_size, minibatch, blank_label,
+                     alpha, beta, log_prob, workspace, workspace_bytes, stream);
 }
 
 ds2ctc_status ds2ctc_loss_sum(const float* costs, int minibatch, double* out2, void* stream) {

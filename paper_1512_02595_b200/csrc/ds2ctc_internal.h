@@ -232,6 +232,18 @@ struct ViterbiArgs {
   int t_max, B, A, blank;
 };
 
+// Full lattice export (ctc_lattice.cu; ctc_lattice, ctc.cpp:145-169). The
+// descriptor's bp_off is the utterance's cell offset into alpha / beta.
+struct LatticeArgs {
+  const float* x;  // [T_max][B][A]
+  const ViterbiDesc* desc;
+  const int* labels;
+  double* alpha;     // sum_b S_b * T_b cells, utterance b row-major [S_b][T_b]
+  double* beta;      // same layout (emission-exclusive beta)
+  double* log_prob;  // [B]
+  int t_max, B, A, blank;
+};
+
 struct ViterbiLayout {
   size_t desc, labels, bp, total;
   int t_max;
@@ -265,5 +277,7 @@ int launch_loss_sum(const float* costs, int B, double* out2, void* stream);
 int read_watchdog(unsigned long long* out4);
 size_t viterbi_smem_bytes(int T, int L);
 int launch_viterbi(const ViterbiArgs& a, size_t smem, void* stream);
+size_t lattice_smem_bytes(int T, int L);
+int launch_lattice(const LatticeArgs& a, size_t smem, void* stream);
 
 }  // namespace ds2ctc

@@ -207,3 +207,63 @@ def viterbi_align(frame_logits, label: Sequence[int], blank: int, device: int = 
     if int(status[0].item()) != 0:
         raise ValueError("viterbi_align: label infeasible for frame count or no feasible path")
     return align[0].cpu().numpy().astype(np.int64).tolist()
+
+
+@dataclass
+class CtcLattice:
+    """asr::ctc::CtcLattice (ctc.hpp:55-60): augmented label, alpha and the
+    emission-exclusive beta as (2L+1) x T fp64 matrices, log p."""
+
+    augmented_label: list
+    alpha: np.ndarray
+    beta: np.ndarray
+    log_prob: float
+
+
+def ctc_lattice_batch(activations, flat_labels, label_lengths, input_lengths, blank: Optional[int] = None,
+                      stream=None):
+    """Batched lattice export on the GPU (ds2ctc_ctc_lattice). Returns
+    (alpha, beta, log_prob) as fp64 CUDA tensors: alpha / beta flat over all
+    utterances' row-major [2L_b+1][T_b] blocks, log_prob [B]."""
+    import torch
+
+    if not (activations.is_cuda and activations.dtype == torch.float32 and activations.is_contiguous()):
+        raise ValueError("activations must be a contiguous float32 CUDA tensor [T, B, A]")
+    T_max, B, A = activations.shape
+    blank = A - 1 if blank is None else int(blank)
+    dev = activations.device
+    ll, il = _i32(label_lengths), _i32(input_lengths)
+    cells, wsb = ctypes.c_size_t(), ctypes.c_size_t()
+    _lib.check(_lib.lib().ds2ctc_lattice_get_sizes(_iptr(ll), _iptr(il), B, ctypes.byref(cells), ctypes.byref(wsb)),
+               "ds2ctc_lattice_get_sizes")
+    alpha = torch.empty(max(int(cells.value), 1), dtype=torch.float64, device=dev)
+    beta = torch.empty_like(alpha)
+    log_prob = torch.empty(max(B, 1), dtype=torch.float64, device=dev)
+    ws = _default_ws.setdefault(dev.index, Workspace(dev))
+    ws_ptr, ws_bytes = ws.get(int(wsb.value))
+    if stream is None:
+        stream = torch.cuda.current_stream(dev)
+    st = _lib.lib().ds2ctc_ctc_lattice(
+        ctypes.c_void_p(activations.data_ptr()), _iptr(_i32(flat_labels)), _iptr(ll), _iptr(il), A, B, blank,
+        ctypes.c_void_p(alpha.data_ptr()), ctypes.c_void_p(beta.data_ptr()), ctypes.c_void_p(log_prob.data_ptr()),
+        ctypes.c_void_p(ws_ptr), ws_bytes, ctypes.c_void_p(stream.cuda_stream))
+    _lib.check(st, "ds2ctc_ctc_lattice")
+    return alpha[:int(cells.value)], beta[:int(cells.value)], log_prob[:B]
+
+
+def ctc_lattice(frame_logits, label: Sequence[int], blank: int, device: int = 0) -> CtcLattice:
+    """Drop-in for asr::ctc::ctc_lattice (ctc.cpp:145-169) on one utterance."""
+    import torch
+
+    x = np.ascontiguousarray(np.asarray(frame_logits, dtype=np.float32))
+    T, A = x.shape
+    lab = [int(c) for c in label]
+    if T < 1:
+        raise ValueError("ctc: need at least one frame")
+    xt = torch.from_numpy(x.reshape(T, 1, A)).to(torch.device("cuda", device))
+    alpha, beta, lp = ctc_lattice_batch(xt, lab, [len(lab)], [T], blank=blank)
+    S = 2 * len(lab) + 1
+    aug = [blank]
+    for c in lab:
+        aug += [c, blank]
+    return CtcLattice(aug, alpha.cpu().numpy().reshape(S, T), beta.cpu().numpy().reshape(S, T), float(lp[0].item()))
