@@ -341,6 +341,24 @@ def main():
                     traffic = json.load(f).get(args.workload)
             except Exception:
                 traffic = None
+        # The binding bound at small alphabets is the serial lattice chain, not HBM
+        # (DESIGN.md §5.1): each CTA of k_pair runs T_max dependent steps. Report the
+        # measured cycles per step beside the isolated-step floor measured by
+        # tools/microbench/chain_step.cu (one chain warp, K label pairs per lane, the
+        # product arithmetic, no service/gradient/halo work), per K of the launch
+        # (pick_K, ds2ctc_internal.h; K=1 and K=8 use the nearest measured K).
+        sm_mhz = (clocks or {}).get("sm_mhz") or 1965.0
+        t_steps = int(il_g.max()) if il_g.size else 0
+        pairs = int(ll_g.max()) + 1 if ll_g.size else 1
+        K = next((k for k in (1, 2, 3, 4, 6, 8) if pairs <= 3 * 28 * k), 8)
+        floor = {1: 186.0, 2: 186.0, 3: 214.0, 4: 285.0, 6: 368.5, 8: 368.5}[K]
+        chain = None
+        if t_steps > 0 and pair_ms > 0:
+            cps = pair_ms * 1e-3 * sm_mhz * 1e6 / t_steps
+            chain = {"bound": "serial lattice chain (T_max dependent steps per CTA)", "steps": t_steps,
+                     "pairs_per_lane": K, "cycles_per_step": cps, "floor_cycles_per_step": floor,
+                     "frac": floor / cps,
+                     "floor_source": "tools/microbench/chain_step.cu (profiles/r01_microbench_chain_step.txt)"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": wl["scaling"],
@@ -352,7 +370,7 @@ def main():
             "stage_ms": {"k_pair": pair_ms, "k_dense": dense_ms, "k_finalize": final_ms},
             "roofline": {"bound": "hbm", "kernel": dom_name, "kernel_ms": dom_ms, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "alg_bytes_per_launch": alg_bytes},
+                         "traffic": traffic, "alg_bytes_per_launch": alg_bytes, "chain": chain},
             "e2e": {"value": total_utts / (e2e_ms / 1e3), "unit": UNIT,
                     "h2d_bytes_per_step": int(acts_h.nbytes + 4 * (ll.sum() + 2 * B)),
                     "d2h_bytes_per_step": int(acts_h.nbytes + 4 * B), "ms_per_step": e2e_ms},
