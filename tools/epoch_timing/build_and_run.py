@@ -21,7 +21,8 @@ def build(defines=()):
     if os.path.exists(so) and all(os.path.getmtime(f) <= os.path.getmtime(so) for f in srcs):
         return so  # prebuilt (e.g. shipped with the snapshot)
     objs = []
-    for src in ("ctc_pair.cu", "ctc_dense.cu"):
+    from paper_1512_02595_b200.build import CU_SOURCES
+    for src in CU_SOURCES:
         obj = os.path.join(OUT, tag + src + ".o")
         subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo",
                         "-DDS2CTC_EPOCH_TIMING", *[f"-DDS2CTC_EXP_{d}" for d in defines], "-Xcompiler", "-fPIC", f"-I{ROOT}/include", f"-I{CSRC}", "-c",
