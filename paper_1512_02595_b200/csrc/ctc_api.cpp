@@ -125,14 +125,20 @@ ds2ctc_status validate(const int* label_lengths, const int* input_lengths, int A
 
 // Builds the metadata blob (int32 words laid out per Layout) into `blob`.
 // Returns (max L, max nkey) over utterances that run the lattice.
+// The key map is packed: key_char (sum nkey words) from lay.key_char, then
+// key_start (sum nkey + B words) right after it; *key_start_off and
+// *meta_used receive that offset and the bytes to copy.
 std::pair<int, int> build_metadata(const Layout& lay, const int* flat_labels, const int* label_lengths,
-                                   const int* input_lengths, int A, int B, int blank, std::vector<int32_t>& blob) {
-  blob.resize(lay.meta_end / sizeof(int32_t));  // every word below is written
+                                   const int* input_lengths, int A, int B, int blank, std::vector<int32_t>& blob,
+                                   size_t* key_start_off, size_t* meta_used) {
+  blob.resize(lay.meta_end / sizeof(int32_t));  // every word below the used prefix is written
   auto* desc = reinterpret_cast<UttDesc*>(blob.data() + lay.desc / 4);
   int* order = blob.data() + lay.order / 4;
   int* labels = blob.data() + lay.labels / 4;
   int* key_char = blob.data() + lay.key_char / 4;
-  int* key_start = blob.data() + lay.key_start / 4;
+  thread_local std::vector<int> key_start_v;
+  key_start_v.resize(static_cast<size_t>(lay.sum_L) + 2 * B + 1);
+  int* key_start = key_start_v.data();
   int* key_pos = blob.data() + lay.key_pos / 4;
   if (lay.sum_L > 0) std::memcpy(labels, flat_labels, sizeof(int) * lay.sum_L);
 
@@ -215,10 +221,14 @@ std::pair<int, int> build_metadata(const Layout& lay, const int* flat_labels, co
       max_nkey = std::max(max_nkey, nkey);
     }
     lab_off += L;
-    key_off += L + 1;
+    key_off += nkey;
     store_off += static_cast<long long>(u.col_w) * (T + 1);
     occ_off += static_cast<long long>(T) * nkey;
   }
+  // key_start right behind the used part of key_char
+  *key_start_off = lay.key_char + sizeof(int) * static_cast<size_t>(key_off);
+  std::memcpy(blob.data() + *key_start_off / 4, key_start, sizeof(int) * static_cast<size_t>(key_off + B));
+  *meta_used = *key_start_off + sizeof(int) * static_cast<size_t>(key_off + B);
   // Longest first (the serial chain is T steps), so long pairs start in the first wave.
   std::iota(order, order + B, 0);
   std::stable_sort(order, order + B, [&](int x, int y) {
@@ -242,15 +252,17 @@ ds2ctc_status run(const float* acts, float* grads, const int* flat_labels, const
   if (reinterpret_cast<uintptr_t>(workspace) % kAlign != 0) return DS2CTC_STATUS_INVALID_VALUE;
 
   thread_local std::vector<int32_t> blob;
-  const auto mx = build_metadata(lay, flat_labels, label_lengths, input_lengths, A, B, blank, blob);
+  size_t key_start_off = 0, meta_used = 0;
+  const auto mx =
+      build_metadata(lay, flat_labels, label_lengths, input_lengths, A, B, blank, blob, &key_start_off, &meta_used);
 
   auto* ws = static_cast<unsigned char*>(workspace);
   auto s = static_cast<cudaStream_t>(stream);
   cudaEvent_t ev = nullptr;
-  void* pinned = staging_for_current_device().acquire(lay.meta_end, &ev);
+  void* pinned = staging_for_current_device().acquire(meta_used, &ev);
   if (pinned == nullptr) return DS2CTC_STATUS_MEMOPS_FAILED;
-  std::memcpy(pinned, blob.data(), lay.meta_end);
-  if (cudaMemcpyAsync(ws, pinned, lay.meta_end, cudaMemcpyHostToDevice, s) != cudaSuccess)
+  std::memcpy(pinned, blob.data(), meta_used);
+  if (cudaMemcpyAsync(ws, pinned, meta_used, cudaMemcpyHostToDevice, s) != cudaSuccess)
     return DS2CTC_STATUS_MEMOPS_FAILED;
   if (cudaEventRecord(ev, s) != cudaSuccess) return DS2CTC_STATUS_MEMOPS_FAILED;
 
@@ -263,7 +275,7 @@ ds2ctc_status run(const float* acts, float* grads, const int* flat_labels, const
   a.order = reinterpret_cast<const int*>(ws + lay.order);
   a.labels = reinterpret_cast<const int*>(ws + lay.labels);
   a.key_char = reinterpret_cast<const int*>(ws + lay.key_char);
-  a.key_start = reinterpret_cast<const int*>(ws + lay.key_start);
+  a.key_start = reinterpret_cast<const int*>(ws + key_start_off);
   a.key_pos = reinterpret_cast<const int*>(ws + lay.key_pos);
   a.store = reinterpret_cast<float*>(ws + lay.store);
   a.occ = fused ? nullptr : reinterpret_cast<float*>(ws + lay.occ);

@@ -38,7 +38,7 @@ struct alignas(16) UttDesc {
   int status;     // 0 = run, 1 = infeasible (T < min_frames), 2 = trivial (T == 0, L == 0: cost 0)
   int lab_off;    // offset into labels[] (also into key_pos[])
   int nkey;       // key slots: slot 0 = blank, slots 1.. = distinct non-blank symbols ascending
-  int key_off;    // offset into key_char[]; key_start has nkey+1 entries at key_off + b
+  int key_off;    // offset into key_char[] (packed); key_start has nkey+1 entries at key_off + b
   int col_w;      // floats per stored lattice column: roundup4(S) + roundup4(chain warps)
   long long store_off;  // offset (floats) into the half-lattice store: col_w * (T + 1)
   long long occ_off;    // offset (floats) into the compact occupancy rows (split path): T * nkey
@@ -178,9 +178,11 @@ inline Layout make_layout(const int* label_lengths, const int* input_lengths, in
   lay.desc = off;      off += sizeof(UttDesc) * B;
   lay.order = off;     off += sizeof(int) * B;
   lay.labels = off;    off += sizeof(int) * sum_L;
+  lay.key_pos = off;   off += sizeof(int) * sum_L;
+  // key_char (sum nkey) then key_start (sum nkey + B), packed at run time from
+  // here: only the used prefix of the blob is copied (nkey <= min(L+1, A))
   lay.key_char = off;  off += sizeof(int) * (sum_L + B);
   lay.key_start = off; off += sizeof(int) * (sum_L + 2 * B);
-  lay.key_pos = off;   off += sizeof(int) * sum_L;
   lay.meta_end = off;
   off = align_up(off);
   lay.store = off;     off = align_up(off + sizeof(float) * static_cast<size_t>(store));
