@@ -130,6 +130,12 @@ ds2ctc_status ds2ctc_viterbi_align(const float* activations, const int* flat_lab
                                    int* alignments, int* status, void* workspace, size_t workspace_bytes,
                                    void* stream);
 
+/* Host-buffer form of ds2ctc_viterbi_align (alignments [minibatch][T_max],
+ * status [minibatch] are HOST arrays); synchronous, on `device`. */
+ds2ctc_status ds2ctc_viterbi_align_host(const float* activations, const int* flat_labels, const int* label_lengths,
+                                        const int* input_lengths, int alphabet_size, int minibatch, int blank_label,
+                                        int* alignments, int* status, int device);
+
 /*
  * Full CTC lattice export, the batched device counterpart
  * of CtcLattice ctc_lattice(const Matrix& frame_logits, const std::vector<int>&
@@ -150,6 +156,12 @@ ds2ctc_status ds2ctc_ctc_lattice(const float* activations, const int* flat_label
                                  const int* input_lengths, int alphabet_size, int minibatch, int blank_label,
                                  double* alpha, double* beta, double* log_prob, void* workspace,
                                  size_t workspace_bytes, void* stream);
+
+/* Host-buffer form of ds2ctc_ctc_lattice (alpha, beta [cells], log_prob
+ * [minibatch] are HOST arrays); synchronous, on `device`. */
+ds2ctc_status ds2ctc_ctc_lattice_host(const float* activations, const int* flat_labels, const int* label_lengths,
+                                      const int* input_lengths, int alphabet_size, int minibatch, int blank_label,
+                                      double* alpha, double* beta, double* log_prob, int device);
 
 /*
  * Per-shard {sum of feasible costs, number of infeasible utterances} as fp64

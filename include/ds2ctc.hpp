@@ -102,6 +102,66 @@ std::vector<double> ctc_loss_batch_gpu(const std::vector<M>& logits, const std::
   return std::vector<double>(costs.begin(), costs.end());
 }
 
+// std::vector<int> asr::ctc::viterbi_align(const Matrix& frame_logprobs,
+//                                          const std::vector<int>& label, int blank)
+// (ctc.hpp:97-101, ctc.cpp:327-370): frame symbols of the best alignment;
+// throws where the reference throws (label infeasible for T, or no path).
+template <class M>
+std::vector<int> viterbi_align_gpu(const M& frame_logits, const std::vector<int>& label, int blank, int device = 0) {
+  const int T = frame_logits.rows();
+  const int A = frame_logits.cols();
+  std::vector<float> x(static_cast<size_t>(T) * A);
+  for (int t = 0; t < T; ++t)
+    for (int k = 0; k < A; ++k) x[static_cast<size_t>(t) * A + k] = static_cast<float>(frame_logits(t, k));
+  const int L = static_cast<int>(label.size());
+  std::vector<int> out(static_cast<size_t>(T > 0 ? T : 1));
+  int status = 1;
+  check(ds2ctc_viterbi_align_host(x.data(), label.data(), &L, &T, A, 1, blank, out.data(), &status, device),
+        "viterbi_align_gpu");
+  if (status != 0) throw std::runtime_error("ds2ctc: viterbi_align: label infeasible for frame count or no path");
+  out.resize(static_cast<size_t>(T));
+  return out;
+}
+
+// asr::ctc::CtcLattice (ctc.hpp:55-60) and ctc_lattice (ctc.cpp:145-169).
+template <class M>
+struct CtcLattice {
+  std::vector<int> augmented_label;
+  M alpha;  // (2L+1) x T
+  M beta;   // (2L+1) x T, emission-exclusive
+  double log_prob = -std::numeric_limits<double>::infinity();
+};
+
+template <class M>
+CtcLattice<M> ctc_lattice_gpu(const M& frame_logits, const std::vector<int>& label, int blank, int device = 0) {
+  const int T = frame_logits.rows();
+  const int A = frame_logits.cols();
+  if (T < 1) throw std::runtime_error("ds2ctc: ctc_lattice: need at least one frame");
+  std::vector<float> x(static_cast<size_t>(T) * A);
+  for (int t = 0; t < T; ++t)
+    for (int k = 0; k < A; ++k) x[static_cast<size_t>(t) * A + k] = static_cast<float>(frame_logits(t, k));
+  const int L = static_cast<int>(label.size());
+  const int S = 2 * L + 1;
+  std::vector<double> a(static_cast<size_t>(S) * T), b(a.size());
+  CtcLattice<M> lat;
+  check(ds2ctc_ctc_lattice_host(x.data(), label.data(), &L, &T, A, 1, blank, a.data(), b.data(), &lat.log_prob,
+                                device),
+        "ctc_lattice_gpu");
+  lat.augmented_label.push_back(blank);
+  for (int c : label) {
+    lat.augmented_label.push_back(c);
+    lat.augmented_label.push_back(blank);
+  }
+  lat.alpha = M(S, T);
+  lat.beta = M(S, T);
+  for (int s = 0; s < S; ++s)
+    for (int t = 0; t < T; ++t) {
+      lat.alpha(s, t) = a[static_cast<size_t>(s) * T + t];
+      lat.beta(s, t) = b[static_cast<size_t>(s) * T + t];
+    }
+  return lat;
+}
+
 }  // namespace ds2ctc
 
 #endif  // DS2CTC_HPP

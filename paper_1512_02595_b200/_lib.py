@@ -35,6 +35,8 @@ EXPORTS = (
     "ds2ctc_viterbi_align",
     "ds2ctc_lattice_get_sizes",
     "ds2ctc_ctc_lattice",
+    "ds2ctc_viterbi_align_host",
+    "ds2ctc_ctc_lattice_host",
     "ds2ctc_profile_enable",
     "ds2ctc_profile_read",
     "ds2ctc_debug_watchdog",
@@ -95,6 +97,12 @@ def lib():
             L.ds2ctc_ctc_lattice.restype = ctypes.c_int
             L.ds2ctc_ctc_lattice.argtypes = [_p, _ip, _ip, _ip, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p, _p, _p,
                                              _p, ctypes.c_size_t, _p]
+            L.ds2ctc_viterbi_align_host.restype = ctypes.c_int
+            L.ds2ctc_viterbi_align_host.argtypes = [_p, _ip, _ip, _ip, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p,
+                                                    _p, ctypes.c_int]
+            L.ds2ctc_ctc_lattice_host.restype = ctypes.c_int
+            L.ds2ctc_ctc_lattice_host.argtypes = [_p, _ip, _ip, _ip, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p, _p,
+                                                  _p, ctypes.c_int]
             L.ds2ctc_viterbi_align.restype = ctypes.c_int
             L.ds2ctc_viterbi_align.argtypes = [_p, _ip, _ip, _ip, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p, _p,
                                                _p, ctypes.c_size_t, _p]

@@ -600,4 +600,87 @@ ds2ctc_status ds2ctc_compute_loss_host(const float* activations, float* gradient
   return DS2CTC_STATUS_SUCCESS;
 }
 
+// Host-buffer forms of the alignment and lattice export (the C++ shim's
+// per-utterance viterbi_align / ctc_lattice): copies through the per-thread
+// device context, synchronous.
+ds2ctc_status ds2ctc_viterbi_align_host(const float* activations, const int* flat_labels, const int* label_lengths,
+                                        const int* input_lengths, int alphabet_size, int minibatch, int blank_label,
+                                        int* alignments, int* status, int device) {
+  ds2ctc_status st = validate(label_lengths, input_lengths, alphabet_size, minibatch, blank_label, flat_labels);
+  if (st != DS2CTC_STATUS_SUCCESS) return st;
+  if (minibatch == 0) return DS2CTC_STATUS_SUCCESS;
+  if (alignments == nullptr || status == nullptr) return DS2CTC_STATUS_INVALID_VALUE;
+  thread_local std::map<int, HostContext> contexts;
+  if (cudaSetDevice(device) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  HostContext& ctx = contexts[device];
+  if (ctx.device < 0) {
+    ctx.device = device;
+    if (cudaStreamCreateWithFlags(&ctx.stream, cudaStreamNonBlocking) != cudaSuccess)
+      return DS2CTC_STATUS_EXECUTION_FAILED;
+  }
+  const ViterbiLayout lay = make_viterbi_layout(label_lengths, input_lengths, minibatch);
+  const size_t elems = static_cast<size_t>(lay.t_max) * minibatch * alphabet_size;
+  const size_t out_bytes = sizeof(int) * (static_cast<size_t>(lay.t_max) * minibatch + minibatch);
+  if (elems > 0 && activations == nullptr) return DS2CTC_STATUS_INVALID_VALUE;
+  if (!grow(&ctx.acts, &ctx.acts_cap, elems * sizeof(float)) || !grow(&ctx.grads, &ctx.grads_cap, out_bytes) ||
+      !grow(&ctx.ws, &ctx.ws_cap, lay.total))
+    return DS2CTC_STATUS_MEMOPS_FAILED;
+  if (elems > 0 &&
+      cudaMemcpyAsync(ctx.acts, activations, elems * sizeof(float), cudaMemcpyHostToDevice, ctx.stream) != cudaSuccess)
+    return DS2CTC_STATUS_MEMOPS_FAILED;
+  int* d_align = static_cast<int*>(ctx.grads);
+  int* d_status = d_align + static_cast<size_t>(lay.t_max) * minibatch;
+  st = run_viterbi(static_cast<const float*>(ctx.acts), flat_labels, label_lengths, input_lengths, alphabet_size,
+                   minibatch, blank_label, d_align, d_status, ctx.ws, ctx.ws_cap, ctx.stream);
+  if (st != DS2CTC_STATUS_SUCCESS) return st;
+  if (cudaMemcpyAsync(alignments, d_align, sizeof(int) * static_cast<size_t>(lay.t_max) * minibatch,
+                      cudaMemcpyDeviceToHost, ctx.stream) != cudaSuccess ||
+      cudaMemcpyAsync(status, d_status, sizeof(int) * minibatch, cudaMemcpyDeviceToHost, ctx.stream) != cudaSuccess)
+    return DS2CTC_STATUS_MEMOPS_FAILED;
+  if (cudaStreamSynchronize(ctx.stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  return DS2CTC_STATUS_SUCCESS;
+}
+
+ds2ctc_status ds2ctc_ctc_lattice_host(const float* activations, const int* flat_labels, const int* label_lengths,
+                                      const int* input_lengths, int alphabet_size, int minibatch, int blank_label,
+                                      double* alpha, double* beta, double* log_prob, int device) {
+  ds2ctc_status st = validate(label_lengths, input_lengths, alphabet_size, minibatch, blank_label, flat_labels);
+  if (st != DS2CTC_STATUS_SUCCESS) return st;
+  if (minibatch == 0) return DS2CTC_STATUS_SUCCESS;
+  if (alpha == nullptr || beta == nullptr || log_prob == nullptr) return DS2CTC_STATUS_INVALID_VALUE;
+  thread_local std::map<int, HostContext> contexts;
+  if (cudaSetDevice(device) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  HostContext& ctx = contexts[device];
+  if (ctx.device < 0) {
+    ctx.device = device;
+    if (cudaStreamCreateWithFlags(&ctx.stream, cudaStreamNonBlocking) != cudaSuccess)
+      return DS2CTC_STATUS_EXECUTION_FAILED;
+  }
+  const ViterbiLayout lay = make_viterbi_layout(label_lengths, input_lengths, minibatch);
+  size_t cells = 0;
+  for (int b = 0; b < minibatch; ++b)
+    cells += static_cast<size_t>(input_lengths[b]) * (2 * static_cast<size_t>(label_lengths[b]) + 1);
+  const size_t elems = static_cast<size_t>(lay.t_max) * minibatch * alphabet_size;
+  if (elems > 0 && activations == nullptr) return DS2CTC_STATUS_INVALID_VALUE;
+  const size_t out_bytes = sizeof(double) * (2 * cells + minibatch);
+  if (!grow(&ctx.acts, &ctx.acts_cap, elems * sizeof(float)) || !grow(&ctx.grads, &ctx.grads_cap, out_bytes) ||
+      !grow(&ctx.ws, &ctx.ws_cap, lay.bp))
+    return DS2CTC_STATUS_MEMOPS_FAILED;
+  if (elems > 0 &&
+      cudaMemcpyAsync(ctx.acts, activations, elems * sizeof(float), cudaMemcpyHostToDevice, ctx.stream) != cudaSuccess)
+    return DS2CTC_STATUS_MEMOPS_FAILED;
+  double* d_alpha = static_cast<double*>(ctx.grads);
+  double* d_beta = d_alpha + cells;
+  double* d_lp = d_beta + cells;
+  st = run_lattice(static_cast<const float*>(ctx.acts), flat_labels, label_lengths, input_lengths, alphabet_size,
+                   minibatch, blank_label, d_alpha, d_beta, d_lp, ctx.ws, ctx.ws_cap, ctx.stream);
+  if (st != DS2CTC_STATUS_SUCCESS) return st;
+  if (cudaMemcpyAsync(alpha, d_alpha, sizeof(double) * cells, cudaMemcpyDeviceToHost, ctx.stream) != cudaSuccess ||
+      cudaMemcpyAsync(beta, d_beta, sizeof(double) * cells, cudaMemcpyDeviceToHost, ctx.stream) != cudaSuccess ||
+      cudaMemcpyAsync(log_prob, d_lp, sizeof(double) * minibatch, cudaMemcpyDeviceToHost, ctx.stream) != cudaSuccess)
+    return DS2CTC_STATUS_MEMOPS_FAILED;
+  if (cudaStreamSynchronize(ctx.stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  return DS2CTC_STATUS_SUCCESS;
+}
+
 }  // extern "C"

@@ -78,6 +78,39 @@ int main() {
                 x.rows(), labels[i].size(), loss, costs[i], rel, gerr, rel1, gerr1);
     if (rel > 1e-4 || gerr > 1e-4 || rel1 > 1e-4 || gerr1 > 1e-4) ++failures;
   }
+  // viterbi_align_gpu / ctc_lattice_gpu (the f2 / f3 drop-ins) vs the oracle
+  for (size_t i = 0; i < 5; ++i) {
+    const Matrix& x = batch[i];
+    const int T = x.rows(), L = static_cast<int>(labels[i].size()), S = 2 * L + 1;
+    std::vector<int> ref(static_cast<size_t>(T));
+    const int rc = orc_viterbi_align(x.data(), T, A, labels[i].data(), L, A - 1, ref.data());
+    try {
+      const std::vector<int> al = ds2ctc::viterbi_align_gpu(x, labels[i], A - 1);
+      if (rc != 0 || al != ref) {
+        std::printf("utt %zu: alignment differs\n", i);
+        ++failures;
+      }
+    } catch (const std::exception& e) {
+      if (rc == 0) {
+        std::printf("utt %zu: unexpected throw %s\n", i, e.what());
+        ++failures;
+      }
+    }
+    std::vector<double> ra(static_cast<size_t>(S) * T), rb(ra.size());
+    double rlp = 0;
+    orc_ctc_lattice(x.data(), T, A, labels[i].data(), L, A - 1, ra.data(), rb.data(), &rlp);
+    const auto lat = ds2ctc::ctc_lattice_gpu(x, labels[i], A - 1);
+    double err = std::fabs(lat.log_prob - rlp);
+    for (int s = 0; s < S; ++s)
+      for (int t = 0; t < T; ++t) {
+        const double r1 = ra[static_cast<size_t>(s) * T + t], r2 = rb[static_cast<size_t>(s) * T + t];
+        if (std::isinf(r1) != std::isinf(lat.alpha(s, t)) || std::isinf(r2) != std::isinf(lat.beta(s, t))) ++failures;
+        if (std::isfinite(r1)) err = std::fmax(err, std::fabs(lat.alpha(s, t) - r1));
+        if (std::isfinite(r2)) err = std::fmax(err, std::fabs(lat.beta(s, t) - r2));
+      }
+    std::printf("utt %zu: viterbi %s, lattice max err %.2e\n", i, rc == 0 ? "aligned" : "none", err);
+    if (err > 1e-9) ++failures;
+  }
   std::printf("%s\n", failures ? "FAIL" : "PASS");
   return failures ? 1 : 0;
 }
