@@ -104,3 +104,31 @@ def test_missing_library_fails_loudly(monkeypatch):
     monkeypatch.setattr(_lib, "LIB_PATH", "/nonexistent/libds2ctc.so")
     with pytest.raises(ImportError):
         _lib.lib()
+
+
+def test_alignment_and_lattice_entry_points_validate_without_gpu():
+    lib = _lib.lib()
+    P = ctypes.POINTER(ctypes.c_int)
+    ll = np.array([2, 3], dtype=np.int32)
+    il = np.array([5, 7], dtype=np.int32)
+    out = ctypes.c_size_t()
+    assert lib.ds2ctc_viterbi_get_workspace_size(ll.ctypes.data_as(P), il.ctypes.data_as(P), 6, 2,
+                                                 ctypes.byref(out)) == 0
+    assert out.value >= 5 * 5 + 7 * 7  # one backpointer byte per lattice cell
+    cells, wsb = ctypes.c_size_t(), ctypes.c_size_t()
+    assert lib.ds2ctc_lattice_get_sizes(ll.ctypes.data_as(P), il.ctypes.data_as(P), 2, ctypes.byref(cells),
+                                        ctypes.byref(wsb)) == 0
+    assert cells.value == 5 * 5 + 7 * 7
+    bad = np.array([-1, 3], dtype=np.int32)
+    assert lib.ds2ctc_viterbi_get_workspace_size(bad.ctypes.data_as(P), il.ctypes.data_as(P), 6, 2,
+                                                 ctypes.byref(out)) == 1
+    # label outside [0, A) and T = 0 for the lattice are rejected before any CUDA call
+    lab = np.array([0, 9, 1, 2, 3], dtype=np.int32)
+    assert lib.ds2ctc_viterbi_align(None, lab.ctypes.data_as(P), ll.ctypes.data_as(P), il.ctypes.data_as(P), 6, 2, 5,
+                                    1, 1, 256, 1 << 20, None) == 1
+    il0 = np.array([0, 7], dtype=np.int32)
+    lab_ok = np.array([0, 1, 1, 2, 3], dtype=np.int32)
+    assert lib.ds2ctc_ctc_lattice(None, lab_ok.ctypes.data_as(P), ll.ctypes.data_as(P), il0.ctypes.data_as(P), 6, 2,
+                                  5, 1, 1, 1, 256, 1 << 20, None) == 1
+    # an empty minibatch is a valid no-op (empty data-parallel shard)
+    assert lib.ds2ctc_viterbi_align(None, None, None, None, 6, 0, 5, None, None, None, 0, None) == 0
