@@ -359,14 +359,24 @@ def main():
         # product arithmetic, no service/gradient/halo work), per K of the launch
         # (pick_K, ds2ctc_internal.h; K=1 and K=8 use the nearest measured K).
         sm_mhz = (clocks or {}).get("sm_mhz") or 1965.0
-        t_steps = int(il_g.max()) if il_g.size else 0
+        # Serial steps of the launch: each utterance is two CTAs of T_b steps
+        # (one per SM); with more CTAs than SMs, the LPT makespan of those
+        # chains over the SMs (the launch order is longest first).
+        import heapq
+
+        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        loads = [0] * n_sm
+        for t_b in sorted((int(v) for v in il for _ in range(2)), reverse=True):
+            heapq.heapreplace(loads, loads[0] + t_b)
+        t_steps = max(loads) if il.size else 0
         pairs = int(ll_g.max()) + 1 if ll_g.size else 1
         K = next((k for k in (1, 2, 3, 4, 6, 8) if pairs <= 3 * 28 * k), 8)
         floor = {1: 186.0, 2: 186.0, 3: 214.0, 4: 285.0, 6: 368.5, 8: 368.5}[K]
         chain = None
         if t_steps > 0 and pair_ms > 0:
             cps = pair_ms * 1e-3 * sm_mhz * 1e6 / t_steps
-            chain = {"bound": "serial lattice chain (T_max dependent steps per CTA)", "steps": t_steps,
+            chain = {"bound": "serial lattice chain (dependent steps per SM: T_max, or the LPT makespan "
+                              "of 2 chains of T_b steps per utterance over the SMs)", "steps": t_steps,
                      "pairs_per_lane": K, "cycles_per_step": cps, "floor_cycles_per_step": floor,
                      "frac": floor / cps,
                      "floor_source": "tools/microbench/chain_step.cu (profiles/r01_microbench_chain_step.txt)"}

@@ -343,6 +343,14 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
 
   // ---- prologue: per-utterance metadata into shared memory ----
   MEET_STAMP(6);
+  if (fused && warp == 0) {  // epoch 0's logit rows (no metadata needed): in flight during the prologue
+    const int n0 = min(P, kmid + 1);
+    const float* xu = a.x + static_cast<size_t>(b) * a.A;
+    for (int c = lane; c < a.A; c += 32)
+      for (int r = 0; r < n0; ++r)
+        cp_async4(xraw + (r & MX) * g.xstride + c, xu + static_cast<size_t>(dir == 0 ? r : T - 1 - r) * rs + c);
+    cp_async_commit();
+  }
   for (int i = tid; i < L; i += NT) s_lab[i] = a.labels[u.lab_off + i];
   for (int j = tid; j < u.nkey; j += NT) s_kchar[j] = a.key_char[u.key_off + j];
   for (int j = tid; j <= u.nkey; j += NT) s_kstart[j] = a.key_start[u.key_off + b + j];
@@ -880,7 +888,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   // ---- prologue staging of epoch 0 ----
   Epoch cur{0, min(P, kmid + 1), 1};
   if (service) {
-    stage(cur);
+    if (!fused) stage(cur);  // fused: issued at the top of the prologue
     cp_async_wait_all();
     __syncwarp();
     convert(cur);
