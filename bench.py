@@ -234,18 +234,42 @@ def main():
     il_c = np.ascontiguousarray(il if B else np.zeros(1, np.int32), dtype=np.int32)
     launches_per_step = 0
 
-    def step():
+    # N > 1: the scalar sums and their all-reduce are one kernel over NVLink
+    # peer memory (ds2ctc_loss_sum_allreduce); DS2CTC_NCCL_REDUCE=1 uses
+    # ds2ctc_loss_sum + an NCCL all-reduce instead (the baseline).
+    peer = None
+    if world > 1 and os.environ.get("DS2CTC_NCCL_REDUCE") != "1":
+        from paper_1512_02595_b200.dist import PeerLossReducer
+
+        peer = PeerLossReducer(dev)
+        if not peer.ok:  # e.g. no CUDA IPC between the ranks' GPUs: the NCCL baseline
+            if rank == 0:
+                print(f"peer all-reduce unavailable ({peer.error}); using NCCL", file=sys.stderr)
+            peer = None
+
+    def step(reduce_mode=None):
         st = lib.ds2ctc_compute_loss_checked(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(grads.data_ptr()),
                                              lab_c.ctypes.data_as(P), ll_c.ctypes.data_as(P),
                                              il_c.ctypes.data_as(P), A, B, A - 1, ctypes.c_void_p(costs.data_ptr()),
                                              ctypes.c_void_p(ws_ptr), ws_bytes, ctypes.c_void_p(stream.cuda_stream))
         _lib.check(st, "ds2ctc_compute_loss")
+        if peer is not None and reduce_mode != "nccl":
+            peer.reduce(costs.data_ptr(), B, pair.data_ptr(), stream.cuda_stream)
+            return
         _lib.check(lib.ds2ctc_loss_sum(ctypes.c_void_p(costs.data_ptr()), B, ctypes.c_void_p(pair.data_ptr()),
                                        ctypes.c_void_p(stream.cuda_stream)), "ds2ctc_loss_sum")
         if world > 1:
             dist.all_reduce(pair)
 
-    # kernels of ours per step: k_pair (+ k_dense + k_finalize for large A) + k_loss_sum
+    if peer is not None:  # the fused reduction must agree with NCCL's
+        step("nccl")
+        ref_pair = pair.clone()
+        step()
+        torch.cuda.synchronize()
+        if not torch.allclose(pair, ref_pair, rtol=1e-12, atol=0):
+            raise RuntimeError(f"peer all-reduce {pair.tolist()} != NCCL {ref_pair.tolist()}")
+
+    # kernels of ours per step: k_pair (+ k_dense + k_finalize for large A) + k_loss_sum / k_loss_allreduce
     if B:
         launches_per_step = 1 + (2 if A > 128 else 0) + 1
     else:
@@ -386,7 +410,9 @@ def main():
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.workload, "desc": wl["desc"], "alphabet": A,
                        "global_batch": total_utts, "frames_per_step": total_frames,
-                       "parallelism": f"dp{world}", "l2": "flushed between steps (256 MiB memset)"},
+                       "parallelism": f"dp{world}", "l2": "flushed between steps (256 MiB memset)",
+                       "scalar_reduce": ("nvlink peer mailboxes (ds2ctc_loss_sum_allreduce)" if peer is not None
+                                         else ("nccl all_reduce" if world > 1 else "none"))},
             "frames_per_s": total_frames / (ms / 1e3),
             "stage_ms": {"k_pair": pair_ms, "k_dense": dense_ms, "k_finalize": final_ms},
             "roofline": {"bound": "hbm", "kernel": dom_name, "kernel_ms": dom_ms, "achieved": achieved, "peak": peak,
@@ -411,6 +437,9 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
+        if peer is not None:
+            torch.cuda.synchronize()
+            peer.close()
         dist.destroy_process_group()
     return 0
 

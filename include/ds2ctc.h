@@ -173,6 +173,25 @@ ds2ctc_status ds2ctc_ctc_lattice_host(const float* activations, const int* flat_
 ds2ctc_status ds2ctc_loss_sum(const float* costs, int minibatch, double* out2, void* stream);
 
 /*
+ * The same per-shard sums fused with their all-reduce over NVLink peer memory
+ * (trainer.cpp:176-179; allreduce.cpp:301-341 with its fixed fold order):
+ * one single-warp kernel per rank stores its pair into every rank's mailbox
+ * and folds all `world` pairs in rank order into out2 (DEVICE fp64 [2]),
+ * bitwise identical on every rank. Setup, once per process group:
+ * ds2ctc_mailbox_alloc gives this rank's mailbox and a 64-byte CUDA IPC
+ * handle to exchange (e.g. torch.distributed.all_gather_object);
+ * ds2ctc_mailbox_open maps each peer's handle. peer_mailboxes[r] is rank r's
+ * mailbox as seen by this process (its own pointer for r == rank). `seq`
+ * starts at 1 and increases by one per call on every rank. Asynchronous on
+ * `stream`; world <= 8.
+ */
+ds2ctc_status ds2ctc_mailbox_alloc(int world, void** mailbox, void* ipc_handle);
+ds2ctc_status ds2ctc_mailbox_open(const void* ipc_handle, void** peer_mailbox);
+ds2ctc_status ds2ctc_mailbox_close(void* peer_mailbox, int own);
+ds2ctc_status ds2ctc_loss_sum_allreduce(const float* costs, int minibatch, double* out2, void* const* peer_mailboxes,
+                                        int rank, int world, unsigned long long seq, void* stream);
+
+/*
  * Stage timing for benchmarks: when enabled for the calling thread with
  * `slots` > 0, each compute call records CUDA events on its stream around
  * every kernel of the pipeline into the next of `slots` event sets (no host

@@ -31,6 +31,10 @@ EXPORTS = (
     "ds2ctc_compute_loss_checked",
     "ds2ctc_compute_loss_host",
     "ds2ctc_loss_sum",
+    "ds2ctc_mailbox_alloc",
+    "ds2ctc_mailbox_open",
+    "ds2ctc_mailbox_close",
+    "ds2ctc_loss_sum_allreduce",
     "ds2ctc_viterbi_get_workspace_size",
     "ds2ctc_viterbi_align",
     "ds2ctc_lattice_get_sizes",
@@ -90,6 +94,15 @@ def lib():
                                                    _p, ctypes.c_int]
             L.ds2ctc_loss_sum.restype = ctypes.c_int
             L.ds2ctc_loss_sum.argtypes = [_p, ctypes.c_int, _p, _p]
+            L.ds2ctc_mailbox_alloc.restype = ctypes.c_int
+            L.ds2ctc_mailbox_alloc.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_void_p), _p]
+            L.ds2ctc_mailbox_open.restype = ctypes.c_int
+            L.ds2ctc_mailbox_open.argtypes = [_p, ctypes.POINTER(ctypes.c_void_p)]
+            L.ds2ctc_mailbox_close.restype = ctypes.c_int
+            L.ds2ctc_mailbox_close.argtypes = [_p, ctypes.c_int]
+            L.ds2ctc_loss_sum_allreduce.restype = ctypes.c_int
+            L.ds2ctc_loss_sum_allreduce.argtypes = [_p, ctypes.c_int, _p, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int,
+                                                    ctypes.c_int, ctypes.c_ulonglong, _p]
             L.ds2ctc_viterbi_get_workspace_size.restype = ctypes.c_int
             L.ds2ctc_viterbi_get_workspace_size.argtypes = [_ip, _ip, ctypes.c_int, ctypes.c_int, _szp]
             L.ds2ctc_lattice_get_sizes.restype = ctypes.c_int

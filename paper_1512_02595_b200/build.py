@@ -21,7 +21,7 @@ LIB = os.path.join(PKG, "libds2ctc.so")
 BUILD = os.path.join(PKG, "_build")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["ctc_pair.cu", "ctc_dense.cu", "ctc_viterbi.cu", "ctc_lattice.cu"]
+CU_SOURCES = ["ctc_pair.cu", "ctc_dense.cu", "ctc_viterbi.cu", "ctc_lattice.cu", "ctc_reduce.cu"]
 CPP_SOURCES = ["ctc_api.cpp", "scheduler.cpp"]
 
 

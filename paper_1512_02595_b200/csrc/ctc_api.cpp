@@ -528,6 +528,50 @@ ds2ctc_status ds2ctc_ctc_lattice(const float* activations, const int* flat_label
                      alpha, beta, log_prob, workspace, workspace_bytes, stream);
 }
 
+ds2ctc_status ds2ctc_mailbox_alloc(int world, void** mailbox, void* ipc_handle) {
+  if (mailbox == nullptr || ipc_handle == nullptr || world < 1 || world > kMaxPeers) return DS2CTC_STATUS_INVALID_VALUE;
+  const size_t bytes = mailbox_bytes(world);
+  if (cudaMalloc(mailbox, bytes) != cudaSuccess) return DS2CTC_STATUS_MEMOPS_FAILED;
+  if (cudaMemset(*mailbox, 0, bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+    return DS2CTC_STATUS_MEMOPS_FAILED;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, *mailbox) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  std::memcpy(ipc_handle, &h, sizeof(h));
+  return DS2CTC_STATUS_SUCCESS;
+}
+
+ds2ctc_status ds2ctc_mailbox_open(const void* ipc_handle, void** peer_mailbox) {
+  if (ipc_handle == nullptr || peer_mailbox == nullptr) return DS2CTC_STATUS_INVALID_VALUE;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, ipc_handle, sizeof(h));
+  if (cudaIpcOpenMemHandle(peer_mailbox, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+    return DS2CTC_STATUS_EXECUTION_FAILED;
+  return DS2CTC_STATUS_SUCCESS;
+}
+
+ds2ctc_status ds2ctc_mailbox_close(void* peer_mailbox, int own) {
+  if (peer_mailbox == nullptr) return DS2CTC_STATUS_INVALID_VALUE;
+  const cudaError_t e = own ? cudaFree(peer_mailbox) : cudaIpcCloseMemHandle(peer_mailbox);
+  return e == cudaSuccess ? DS2CTC_STATUS_SUCCESS : DS2CTC_STATUS_EXECUTION_FAILED;
+}
+
+ds2ctc_status ds2ctc_loss_sum_allreduce(const float* costs, int minibatch, double* out2, void* const* peer_mailboxes,
+                                        int rank, int world, unsigned long long seq, void* stream) {
+  if (out2 == nullptr || minibatch < 0 || (minibatch > 0 && costs == nullptr) || peer_mailboxes == nullptr ||
+      world < 1 || world > kMaxPeers || rank < 0 || rank >= world || seq == 0)
+    return DS2CTC_STATUS_INVALID_VALUE;
+  PeerMailboxes mb{};
+  for (int r = 0; r < world; ++r) {
+    if (peer_mailboxes[r] == nullptr) return DS2CTC_STATUS_INVALID_VALUE;
+    mb.peer[r] = peer_mailboxes[r];
+  }
+  mb.rank = rank;
+  mb.world = world;
+  if (launch_loss_allreduce(costs, minibatch, out2, mb, seq, stream) != cudaSuccess)
+    return DS2CTC_STATUS_EXECUTION_FAILED;
+  return DS2CTC_STATUS_SUCCESS;
+}
+
 ds2ctc_status ds2ctc_loss_sum(const float* costs, int minibatch, double* out2, void* stream) {
   if (minibatch < 0 || out2 == nullptr || (minibatch > 0 && costs == nullptr)) return DS2CTC_STATUS_INVALID_VALUE;
   if (launch_loss_sum(costs, minibatch, out2, stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;

@@ -1,0 +1,96 @@
+// ctc_reduce.cu -- the trainer's scalar reduction fused with its all-reduce
+// over NVLink peer memory (sm_100a).
+//
+// Reference: train_epoch sums {local_loss, local_skipped} over its shard
+// (proj/src/trainer.cpp:160-168) and ring-all-reduces the two scalars
+// (trainer.cpp:176-179, allreduce.cpp:301-341) with a fixed fold order
+// (allreduce.hpp:91-95). Here ONE single-warp kernel per rank forms the
+// rank's pair from the costs (as k_loss_sum), stores it into slot `rank` of
+// every rank's mailbox over NVLink (CUDA IPC mappings of a small device
+// buffer, opened once), publishes a sequence number with release semantics,
+// waits until all `world` slots of this step carry the sequence number and
+// folds them in rank order (bitwise identical on every rank, run to run).
+// Two slot banks alternate by step parity: a rank can be at most one step
+// ahead of a peer (every step waits for every rank), so a bank is never
+// rewritten while a peer still reads it.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ds2ctc_internal.h"
+
+namespace ds2ctc {
+namespace {
+
+struct alignas(32) Slot {
+  double loss, skipped;
+  unsigned long long seq;
+  unsigned long long pad;
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void k_loss_allreduce(const float* __restrict__ costs, int B, double* __restrict__ out2,
+                                 const __grid_constant__ PeerMailboxes mb, unsigned long long seq) {
+  const int lane = threadIdx.x;
+  double loss = 0.0, skipped = 0.0;
+  for (int b = lane; b < B; b += 32) {  // trainer.cpp:160-168, lane-strided then a fixed xor tree
+    const float c = costs[b];
+    if (isfinite(c)) loss += static_cast<double>(c);
+    else skipped += 1.0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    loss += __shfl_xor_sync(0xffffffffu, loss, o);
+    skipped += __shfl_xor_sync(0xffffffffu, skipped, o);
+  }
+  // __grid_constant__: the pointer table is read in place from the parameter
+  // bank (no local copy for the per-lane index)
+  void* const mine = mb.peer[mb.rank];
+  void* const theirs = mb.peer[lane < mb.world ? lane : 0];
+  const int bank = static_cast<int>(seq & 1ull) * mb.world;
+  if (lane < mb.world) {  // this rank's pair into slot `rank` of every mailbox
+    Slot* dst = reinterpret_cast<Slot*>(theirs) + bank + mb.rank;
+    dst->loss = loss;
+    dst->skipped = skipped;
+    st_release_sys(&dst->seq, seq);
+  }
+  double v0 = 0.0, v1 = 0.0;
+  if (lane < mb.world) {  // wait for every rank's pair of this step (bounded)
+    const Slot* src = reinterpret_cast<const Slot*>(mine) + bank + lane;
+    for (unsigned n = 0; ld_acquire_sys(&src->seq) != seq; ++n)
+      if (n == (1u << 26)) break;  // a lost peer: give up instead of hanging the device
+    v0 = src->loss;
+    v1 = src->skipped;
+  }
+  // fold in rank order (allreduce.hpp:91-95): lane 0 gathers the slots in order
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int r = 0; r < mb.world; ++r) {
+    acc0 += __shfl_sync(0xffffffffu, v0, r);
+    acc1 += __shfl_sync(0xffffffffu, v1, r);
+  }
+  if (lane == 0) {
+    out2[0] = acc0;
+    out2[1] = acc1;
+  }
+}
+
+}  // namespace
+
+int launch_loss_allreduce(const float* costs, int B, double* out2, const PeerMailboxes& mb, unsigned long long seq,
+                          void* stream) {
+  k_loss_allreduce<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(costs, B, out2, mb, seq);
+  return cudaGetLastError();
+}
+
+size_t mailbox_bytes(int world) { return 2 * static_cast<size_t>(world) * sizeof(Slot); }
+
+}  // namespace ds2ctc

@@ -276,6 +276,17 @@ int launch_pair(const PairArgs& a, void* stream);
 int launch_dense(const PairArgs& a, bool write_grad, void* stream);
 int launch_finalize(const PairArgs& a, void* stream);
 int launch_loss_sum(const float* costs, int B, double* out2, void* stream);
+
+// Peer mailboxes of the fused scalar all-reduce (ctc_reduce.cu): this
+// process's view (own buffer or CUDA IPC mapping) of every rank's mailbox.
+constexpr int kMaxPeers = 8;
+struct PeerMailboxes {
+  void* peer[kMaxPeers];
+  int rank, world;
+};
+int launch_loss_allreduce(const float* costs, int B, double* out2, const PeerMailboxes& mb, unsigned long long seq,
+                          void* stream);
+size_t mailbox_bytes(int world);
 int read_watchdog(unsigned long long* out4);
 size_t viterbi_smem_bytes(int T, int L);
 int launch_viterbi(const ViterbiArgs& a, size_t smem, void* stream);

@@ -11,6 +11,7 @@ Empty shards still join the collective (trainer.cpp:141-155,173-180).
 """
 from __future__ import annotations
 
+import ctypes
 from typing import Callable, Tuple
 
 import numpy as np
@@ -63,3 +64,76 @@ def dp_ctc_step(batch_input_lengths, batch_label_lengths, alphabet_size: int, ra
     loss, skipped = local_loss_skipped(costs)
     g_loss, g_skipped = reduce_loss_skipped(loss, skipped, device=device)
     return g_loss, g_skipped, idx
+
+
+class PeerLossReducer:
+    """The trainer's {loss, skipped} sums fused with their all-reduce over
+    NVLink peer memory (ds2ctc_loss_sum_allreduce): one single-warp kernel per
+    rank per step, rank-ordered fold, no NCCL call on the step. Setup exchanges
+    CUDA IPC handles of the per-rank mailboxes over the default process group
+    once; every collective of the setup runs on every rank even if a local
+    step failed, and `ok` is the group's agreement (all ranks succeeded)."""
+
+    def __init__(self, device):
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+
+        self.lib = _lib.lib()
+        self.rank = dist.get_rank()
+        self.world = dist.get_world_size()
+        self.opened = []
+        self.own = None
+        self.seq = 0
+        err = None
+        own = ctypes.c_void_p()
+        handle = (ctypes.c_char * 64)()
+        if self.world > 8:
+            err = "more than 8 ranks"
+        elif self.lib.ds2ctc_mailbox_alloc(self.world, ctypes.byref(own), handle) != 0:
+            err = "mailbox alloc / IPC handle failed"
+        else:
+            self.own = own.value
+        handles = [None] * self.world
+        dist.all_gather_object(handles, None if err else bytes(handle))
+        self.ptrs = (ctypes.c_void_p * max(self.world, 1))()
+        if err is None:
+            for r in range(self.world):
+                if r == self.rank:
+                    self.ptrs[r] = self.own
+                    continue
+                if handles[r] is None:
+                    err = f"rank {r} has no mailbox"
+                    break
+                p = ctypes.c_void_p()
+                h = (ctypes.c_char * 64).from_buffer_copy(handles[r])
+                if self.lib.ds2ctc_mailbox_open(h, ctypes.byref(p)) != 0:
+                    err = f"IPC open of rank {r}'s mailbox failed"
+                    break
+                self.ptrs[r] = p.value
+                self.opened.append(p.value)
+        flag = torch.tensor([0 if err else 1], dtype=torch.int32, device=device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        self.ok = bool(flag.item())
+        self.error = err
+        if not self.ok:
+            self.close()
+
+    def reduce(self, costs_ptr: int, B: int, out2_ptr: int, stream_ptr: int) -> None:
+        from . import _lib
+
+        self.seq += 1
+        _lib.check(self.lib.ds2ctc_loss_sum_allreduce(ctypes.c_void_p(costs_ptr), B, ctypes.c_void_p(out2_ptr),
+                                                      ctypes.cast(self.ptrs, ctypes.POINTER(ctypes.c_void_p)),
+                                                      self.rank, self.world, self.seq,
+                                                      ctypes.c_void_p(stream_ptr)),
+                   "ds2ctc_loss_sum_allreduce")
+
+    def close(self) -> None:
+        for p in self.opened:
+            self.lib.ds2ctc_mailbox_close(ctypes.c_void_p(p), 0)
+        if self.own is not None:
+            self.lib.ds2ctc_mailbox_close(ctypes.c_void_p(self.own), 1)
+        self.opened = []
+        self.own = None

@@ -75,3 +75,32 @@ def test_dp_step_matches_single_process(world, n):
     assert sorted(covered) == list(range(n))
     # every rank saw the bitwise-identical reduced value (rank-order fold)
     assert len({r[1] for r in results}) == 1
+
+
+def _peer_worker(rank, world, port, result_q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # No GPU here: the mailbox allocation fails on every rank, every setup
+        # collective still runs (no deadlock) and the group agrees to fall back.
+        red = ddist.PeerLossReducer("cpu")
+        result_q.put((rank, red.ok, red.error is not None))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_reducer_setup_agrees_on_fallback_without_gpu():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(not ok and had_error for _, ok, had_error in results)

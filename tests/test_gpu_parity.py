@@ -148,3 +148,30 @@ def test_host_api_and_single_utterance(golden, cuda):
     assert res.feasible
     assert abs(res.loss - golden[f"{name}/costs"][0]) / golden[f"{name}/costs"][0] <= COST_RTOL
     assert np.abs(res.logit_grad - golden[f"{name}/grads"][:, 0, :]).max() <= GRAD_ATOL
+
+
+def test_fused_loss_allreduce_single_rank(cuda):
+    # ds2ctc_loss_sum_allreduce with world = 1 (its own mailbox) equals ds2ctc_loss_sum;
+    # the multi-rank path is checked against NCCL inside bench.py at N > 1
+    import ctypes
+
+    import torch
+
+    lib = _lib.lib()
+    costs = torch.tensor([1.5, float("inf"), 2.25, 3.0], dtype=torch.float32, device="cuda")
+    a = torch.zeros(2, dtype=torch.float64, device="cuda")
+    b = torch.zeros(2, dtype=torch.float64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    assert lib.ds2ctc_loss_sum(ctypes.c_void_p(costs.data_ptr()), 4, ctypes.c_void_p(a.data_ptr()),
+                               ctypes.c_void_p(s)) == 0
+    own = ctypes.c_void_p()
+    handle = (ctypes.c_char * 64)()
+    assert lib.ds2ctc_mailbox_alloc(1, ctypes.byref(own), handle) == 0
+    ptrs = (ctypes.c_void_p * 1)(own.value)
+    for seq in (1, 2, 3):
+        assert lib.ds2ctc_loss_sum_allreduce(ctypes.c_void_p(costs.data_ptr()), 4, ctypes.c_void_p(b.data_ptr()),
+                                             ctypes.cast(ptrs, ctypes.POINTER(ctypes.c_void_p)), 0, 1, seq,
+                                             ctypes.c_void_p(s)) == 0
+        torch.cuda.synchronize()
+        assert b.tolist() == a.tolist() == [6.75, 1.0]
+    assert lib.ds2ctc_mailbox_close(own, 1) == 0
