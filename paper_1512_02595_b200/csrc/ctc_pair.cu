@@ -1047,10 +1047,14 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   // drain: the last two epochs' gradient rows (grad_occ runs one epoch behind
   // the chain, grad_write two); CTA-uniform condition
   if (!dead && want_grad) {
-    if (grad_warp) grad_occ(prev, (ep - 1) & 1);
+    // the gradient warp finishes the last epoch itself (its label sums are
+    // its own writes), the service warp the one before, concurrently
+    if (grad_warp) {
+      grad_occ(prev, (ep - 1) & 1);
+      __syncwarp();
+      grad_write(prev, (ep - 1) & 1);
+    }
     if (service) grad_write(prev2, (ep - 2) & 1);
-    __syncthreads();
-    if (service) grad_write(prev, (ep - 1) & 1);
     __syncthreads();
   }
 
