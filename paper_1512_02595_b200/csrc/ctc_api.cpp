@@ -50,7 +50,7 @@ class Staging {
   }
 
  private:
-  static constexpr int kSlots = 4;
+  static constexpr int kSlots = 8;
   struct Slot {
     void* ptr = nullptr;
     size_t cap = 0;
@@ -408,6 +408,25 @@ ds2ctc_status run_viterbi(const float* acts, const int* flat_labels, const int* 
 }
 
 // Per-thread device context of the host-buffer entry point.
+// The host-buffer loss call splits the batch into up to this many contiguous
+// sub-batches, each on its own stream, so that chunk c's kernels overlap chunk
+// c+1's host->device copy and chunk c-1's device->host copy (PCIe, not the
+// kernels, bounds this call: DESIGN.md section 8). DS2CTC_HOST_CHUNKS=1
+// restores the single-stream call.
+constexpr int kHostChunksMax = 8;
+
+int host_chunks(int B, size_t bytes) {
+  static const int env = [] {
+    const char* v = std::getenv("DS2CTC_HOST_CHUNKS");
+    return v ? std::atoi(v) : -1;
+  }();
+  // measured on B200: 4 chunks best at the English
+  // shape (5 MB), 8 at the Mandarin one (537 MB)
+  const int dflt = bytes >= (size_t{64} << 20) ? 8 : bytes >= (size_t{1} << 20) ? 4 : 1;
+  int n = env > 0 ? std::min(env, kHostChunksMax) : dflt;
+  return std::max(1, std::min(n, B / 4 > 0 ? B / 4 : 1));
+}
+
 struct HostContext {
   int device = -1;
   cudaStream_t stream = nullptr;
@@ -419,6 +438,8 @@ struct HostContext {
   size_t costs_cap = 0;
   void* ws = nullptr;
   size_t ws_cap = 0;
+  // extra streams of the chunked host pipeline (ds2ctc_compute_loss_host)
+  cudaStream_t chunk_streams[kHostChunksMax - 1] = {};
   ~HostContext() {
     if (device < 0) return;
     cudaSetDevice(device);
@@ -427,6 +448,8 @@ struct HostContext {
     cudaFree(costs);
     cudaFree(ws);
     if (stream) cudaStreamDestroy(stream);
+    for (cudaStream_t cs : chunk_streams)
+      if (cs) cudaStreamDestroy(cs);
   }
 };
 
@@ -621,26 +644,71 @@ ds2ctc_status ds2ctc_compute_loss_host(const float* activations, float* gradient
     if (cudaStreamCreateWithFlags(&ctx.stream, cudaStreamNonBlocking) != cudaSuccess)
       return DS2CTC_STATUS_EXECUTION_FAILED;
   }
-  const Layout lay = make_layout(label_lengths, input_lengths, alphabet_size, minibatch);
-  const size_t elems = static_cast<size_t>(lay.t_max) * minibatch * alphabet_size;
+  const int A = alphabet_size, B = minibatch;
+  const Layout lay = make_layout(label_lengths, input_lengths, A, B);
+  const size_t elems = static_cast<size_t>(lay.t_max) * B * A;
   if (elems > 0 && activations == nullptr) return DS2CTC_STATUS_INVALID_VALUE;
-  if (!grow(&ctx.acts, &ctx.acts_cap, elems * sizeof(float)) ||
-      !grow(&ctx.grads, &ctx.grads_cap, gradients ? elems * sizeof(float) : 0) ||
-      !grow(&ctx.costs, &ctx.costs_cap, minibatch * sizeof(float)) || !grow(&ctx.ws, &ctx.ws_cap, lay.total))
+
+  // Chunk c = utterances [b0[c], b0[c+1]): its activations land compactly as
+  // [T_c][B_c][A] (T_c = the chunk's longest utterance) at a 256-byte aligned
+  // offset, with a workspace of its own.
+  const int nc = host_chunks(B, elems * sizeof(float));
+  int b0[kHostChunksMax + 1];
+  int t_c[kHostChunksMax];
+  size_t lab0[kHostChunksMax], x_off[kHostChunksMax], ws_off[kHostChunksMax + 1];
+  size_t x_total = 0, lab = 0;
+  ws_off[0] = 0;
+  for (int c = 0; c <= nc; ++c) b0[c] = static_cast<int>(static_cast<long long>(B) * c / nc);
+  for (int c = 0; c < nc; ++c) {
+    const int bc = b0[c + 1] - b0[c];
+    t_c[c] = 0;
+    lab0[c] = lab;
+    for (int b = b0[c]; b < b0[c + 1]; ++b) {
+      t_c[c] = std::max(t_c[c], input_lengths[b]);
+      lab += static_cast<size_t>(label_lengths[b]);
+    }
+    x_off[c] = x_total;
+    x_total += (static_cast<size_t>(t_c[c]) * bc * A * sizeof(float) + kAlign - 1) / kAlign * kAlign;
+    const size_t wsz = nc == 1 ? lay.total : make_layout(label_lengths + b0[c], input_lengths + b0[c], A, bc).total;
+    ws_off[c + 1] = ws_off[c] + (wsz + kAlign - 1) / kAlign * kAlign;
+  }
+  if (!grow(&ctx.acts, &ctx.acts_cap, x_total) || !grow(&ctx.grads, &ctx.grads_cap, gradients ? x_total : 0) ||
+      !grow(&ctx.costs, &ctx.costs_cap, B * sizeof(float)) || !grow(&ctx.ws, &ctx.ws_cap, ws_off[nc]))
     return DS2CTC_STATUS_MEMOPS_FAILED;
-  if (elems > 0 &&
-      cudaMemcpyAsync(ctx.acts, activations, elems * sizeof(float), cudaMemcpyHostToDevice, ctx.stream) != cudaSuccess)
-    return DS2CTC_STATUS_MEMOPS_FAILED;
-  st = run(static_cast<const float*>(ctx.acts), gradients ? static_cast<float*>(ctx.grads) : nullptr, flat_labels,
-           label_lengths, input_lengths, alphabet_size, minibatch, blank_label, static_cast<float*>(ctx.costs), ctx.ws,
-           ctx.ws_cap, true, ctx.stream);
-  if (st != DS2CTC_STATUS_SUCCESS) return st;
-  if (gradients && elems > 0 &&
-      cudaMemcpyAsync(gradients, ctx.grads, elems * sizeof(float), cudaMemcpyDeviceToHost, ctx.stream) != cudaSuccess)
-    return DS2CTC_STATUS_MEMOPS_FAILED;
-  if (cudaMemcpyAsync(costs, ctx.costs, minibatch * sizeof(float), cudaMemcpyDeviceToHost, ctx.stream) != cudaSuccess)
-    return DS2CTC_STATUS_MEMOPS_FAILED;
-  if (cudaStreamSynchronize(ctx.stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  for (int c = 1; c < nc; ++c)
+    if (!ctx.chunk_streams[c - 1] &&
+        cudaStreamCreateWithFlags(&ctx.chunk_streams[c - 1], cudaStreamNonBlocking) != cudaSuccess)
+      return DS2CTC_STATUS_EXECUTION_FAILED;
+
+  const size_t row = static_cast<size_t>(B) * A * sizeof(float);
+  for (int c = 0; c < nc; ++c) {
+    cudaStream_t sc = c == 0 ? ctx.stream : ctx.chunk_streams[c - 1];
+    const int bc = b0[c + 1] - b0[c];
+    const size_t w = static_cast<size_t>(bc) * A * sizeof(float);
+    auto* xd = static_cast<unsigned char*>(ctx.acts) + x_off[c];
+    auto* gd = gradients ? static_cast<unsigned char*>(ctx.grads) + x_off[c] : nullptr;
+    const auto* xh = reinterpret_cast<const unsigned char*>(activations) + static_cast<size_t>(b0[c]) * A * sizeof(float);
+    if (t_c[c] > 0 && w > 0 &&
+        cudaMemcpy2DAsync(xd, w, xh, row, w, t_c[c], cudaMemcpyHostToDevice, sc) != cudaSuccess)
+      return DS2CTC_STATUS_MEMOPS_FAILED;
+    float* cd = static_cast<float*>(ctx.costs) + b0[c];
+    st = run(reinterpret_cast<const float*>(xd), reinterpret_cast<float*>(gd), flat_labels + lab0[c],
+             label_lengths + b0[c], input_lengths + b0[c], A, bc, blank_label, cd,
+             static_cast<unsigned char*>(ctx.ws) + ws_off[c], ws_off[c + 1] - ws_off[c], true, sc);
+    if (st != DS2CTC_STATUS_SUCCESS) return st;
+    if (gradients && t_c[c] > 0 && w > 0) {
+      auto* gh = reinterpret_cast<unsigned char*>(gradients) + static_cast<size_t>(b0[c]) * A * sizeof(float);
+      if (cudaMemcpy2DAsync(gh, row, gd, w, w, t_c[c], cudaMemcpyDeviceToHost, sc) != cudaSuccess)
+        return DS2CTC_STATUS_MEMOPS_FAILED;
+      // frames past this chunk's longest utterance: zero rows (the contract), on the host
+      for (int t = t_c[c]; t < lay.t_max; ++t) std::memset(gh + static_cast<size_t>(t) * row, 0, w);
+    }
+    if (bc > 0 && cudaMemcpyAsync(costs + b0[c], cd, bc * sizeof(float), cudaMemcpyDeviceToHost, sc) != cudaSuccess)
+      return DS2CTC_STATUS_MEMOPS_FAILED;
+  }
+  for (int c = 0; c < nc; ++c)
+    if (cudaStreamSynchronize(c == 0 ? ctx.stream : ctx.chunk_streams[c - 1]) != cudaSuccess)
+      return DS2CTC_STATUS_EXECUTION_FAILED;
   return DS2CTC_STATUS_SUCCESS;
 }
 

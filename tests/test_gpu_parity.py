@@ -121,6 +121,32 @@ def test_geometry_variants_vs_oracle(cuda, A, T, L, B):
     assert_parity(costs, grads, rc, rg, il, f"A{A}T{T}L{L}")
 
 
+def test_edge_sweep_max_size_vs_oracle(cuda):
+    # SURVEY.md §8(d) config 5 at one GPU's share: B = 128 at T_max = 1500,
+    # with all-repeat labels (min_frames = 2L-1, exactly feasible and one frame
+    # short), empty labels, L = 300 at T = 1500, and -inf logit rows mixed in
+    B, A = 128, 29
+    T = np.full(B, 1500, dtype=np.int32)
+    L = np.full(B, 300, dtype=np.int32)
+    T[1::4] = np.arange(50, 50 + 32 * 40, 40)[: len(T[1::4])]
+    L[1::4] = np.minimum(300, T[1::4] // 2)
+    L[2], L[3] = 0, 0
+    acts, flat, ll, il = make_batch(A, T, L, seed=505)
+    offs = np.concatenate([[0], np.cumsum(ll)])
+    # utterance 4: 300 copies of one symbol needs 599 frames; give it exactly 599
+    # utterance 12: the same label with 598 frames (infeasible)
+    for b, t in ((4, 599), (12, 598)):
+        flat[offs[b]:offs[b + 1]] = 7
+        il[b] = t
+    acts[:, 6, :] = np.where(np.arange(A) == A - 1, acts[:, 6, :], -np.inf)  # only blank possible
+    acts[:, 8, 3] = -np.inf                                                   # one symbol impossible
+    acts[il.max():] = 0
+    costs, grads = run_gpu(acts, flat, ll, il)
+    rc, rg = oracle.oracle_batch(acts, flat, ll, il, nthreads=8)
+    assert not np.isfinite(rc[12]) and np.isfinite(rc[4]) and np.isfinite(rc[2])
+    assert_parity(costs, grads, rc, rg, il, "edge-max")
+
+
 def test_gradient_rows_sum_to_zero_full_size(cuda):
     # sum_c softmax - sum_c occupancy = 1 - 1 per live frame (size-independent property)
     acts, flat, ll, il = fixed_shape_batch(29, 700, 150, 64, seed=3)
@@ -148,6 +174,28 @@ def test_host_api_and_single_utterance(golden, cuda):
     assert res.feasible
     assert abs(res.loss - golden[f"{name}/costs"][0]) / golden[f"{name}/costs"][0] <= COST_RTOL
     assert np.abs(res.logit_grad - golden[f"{name}/grads"][:, 0, :]).max() <= GRAD_ATOL
+
+
+def test_host_api_chunked_ragged_vs_oracle(cuda):
+    # > 1 MiB of activations: the host call runs as 4 sub-batches on 4 streams;
+    # lengths sorted descending so later chunks are shorter than T_max (their
+    # trailing rows are zeroed on the host), plus an infeasible and an empty label
+    T, L = sortagrad_lengths(32, seed=21)
+    order = np.argsort(-T, kind="stable")
+    T, L = T[order].copy(), L[order].copy()
+    L[-1] = 0
+    acts, flat, ll, il = make_batch(29, T, L, seed=31)
+    offs = np.concatenate([[0], np.cumsum(ll)])
+    flat[offs[20]:offs[21]] = 4
+    il[20] = max(1, 2 * int(ll[20]) - 2)   # one frame short of min_frames = 2L-1
+    assert acts.nbytes >= (1 << 20)
+    grads = np.full_like(acts, np.nan)     # every element must be written
+    costs, grads = dctc.compute_ctc_loss_host(acts, flat, ll, il, gradients=grads)
+    rc, rg = oracle.oracle_batch(acts, flat, ll, il, nthreads=8)
+    assert not np.isfinite(rc[20])
+    assert_parity(costs.astype(np.float64), grads, rc, rg, il, "host-chunked")
+    c2, _ = dctc.compute_ctc_loss_host(acts, flat, ll, il, want_grad=False)
+    assert_parity(c2.astype(np.float64), None, rc, None, il, "host-chunked-cost-only")
 
 
 def test_fused_loss_allreduce_single_rank(cuda):
