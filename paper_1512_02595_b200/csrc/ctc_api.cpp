@@ -241,7 +241,7 @@ std::pair<int, int> build_metadata(const Layout& lay, const int* flat_labels, co
 
 ds2ctc_status run(const float* acts, float* grads, const int* flat_labels, const int* label_lengths,
                   const int* input_lengths, int A, int B, int blank, float* costs, void* workspace,
-                  size_t workspace_bytes, bool check_ws, void* stream) {
+                  size_t workspace_bytes, bool check_ws, void* stream, int ld = 0) {
   ds2ctc_status st = validate(label_lengths, input_lengths, A, B, blank, flat_labels);
   if (st != DS2CTC_STATUS_SUCCESS) return st;
   if (B == 0) return DS2CTC_STATUS_SUCCESS;
@@ -286,6 +286,8 @@ ds2ctc_status run(const float* acts, float* grads, const int* flat_labels, const
   a.B = B;
   a.A = A;
   a.blank = blank;
+  a.ld = ld > 0 ? ld : B;
+  if (a.ld != B && !fused) return DS2CTC_STATUS_INVALID_VALUE;  // k_dense / k_finalize index rows as t*B+b
   int max_L_all = 0;
   for (int b = 0; b < B; ++b) max_L_all = std::max(max_L_all, label_lengths[b]);
   a.g = make_geometry(max_L_all, mx.first, mx.second, A, fused);
@@ -425,6 +427,16 @@ int host_chunks(int B, size_t bytes) {
   const int dflt = bytes >= (size_t{64} << 20) ? 8 : bytes >= (size_t{1} << 20) ? 4 : 1;
   int n = env > 0 ? std::min(env, kHostChunksMax) : dflt;
   return std::max(1, std::min(n, B / 4 > 0 ? B / 4 : 1));
+}
+
+bool host_direct_enabled() {
+  static const bool on = [] {
+    // opt-in: measured equal at the English shape (the PCIe stores stretch
+    // k_pair by what they save) and 6 % slower on SortaGrad
+    const char* v = std::getenv("DS2CTC_HOST_DIRECT");
+    return v != nullptr && std::atoi(v) != 0;
+  }();
+  return on;
 }
 
 struct HostContext {
@@ -653,6 +665,21 @@ ds2ctc_status ds2ctc_compute_loss_host(const float* activations, float* gradient
   // [T_c][B_c][A] (T_c = the chunk's longest utterance) at a 256-byte aligned
   // offset, with a workspace of its own.
   const int nc = host_chunks(B, elems * sizeof(float));
+  // Direct mode (DS2CTC_HOST_DIRECT=1): a page-locked (UVA-mapped) gradient buffer on the fused path
+  // (A <= 128) is written by k_pair itself over PCIe as the rows are produced,
+  // so no device->host gradient copy trails the kernels. The activations then
+  // land in a full [T][B][A] device buffer (chunk c's columns), and each chunk
+  // runs as a sub-batch view with frame stride B.
+  float* g_direct = nullptr;
+  if (gradients && alphabet_size <= kFusedMaxAlphabet && host_direct_enabled()) {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, gradients) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+        pa.devicePointer != nullptr)
+      g_direct = static_cast<float*>(pa.devicePointer);
+    else
+      cudaGetLastError();
+  }
+  const bool direct = g_direct != nullptr;
   int b0[kHostChunksMax + 1];
   int t_c[kHostChunksMax];
   size_t lab0[kHostChunksMax], x_off[kHostChunksMax], ws_off[kHostChunksMax + 1];
@@ -667,12 +694,18 @@ ds2ctc_status ds2ctc_compute_loss_host(const float* activations, float* gradient
       t_c[c] = std::max(t_c[c], input_lengths[b]);
       lab += static_cast<size_t>(label_lengths[b]);
     }
-    x_off[c] = x_total;
-    x_total += (static_cast<size_t>(t_c[c]) * bc * A * sizeof(float) + kAlign - 1) / kAlign * kAlign;
+    if (direct) {
+      x_off[c] = static_cast<size_t>(b0[c]) * A * sizeof(float);
+      x_total = elems * sizeof(float);
+    } else {
+      x_off[c] = x_total;
+      x_total += (static_cast<size_t>(t_c[c]) * bc * A * sizeof(float) + kAlign - 1) / kAlign * kAlign;
+    }
     const size_t wsz = nc == 1 ? lay.total : make_layout(label_lengths + b0[c], input_lengths + b0[c], A, bc).total;
     ws_off[c + 1] = ws_off[c] + (wsz + kAlign - 1) / kAlign * kAlign;
   }
-  if (!grow(&ctx.acts, &ctx.acts_cap, x_total) || !grow(&ctx.grads, &ctx.grads_cap, gradients ? x_total : 0) ||
+  if (!grow(&ctx.acts, &ctx.acts_cap, x_total) ||
+      !grow(&ctx.grads, &ctx.grads_cap, gradients && !direct ? x_total : 0) ||
       !grow(&ctx.costs, &ctx.costs_cap, B * sizeof(float)) || !grow(&ctx.ws, &ctx.ws_cap, ws_off[nc]))
     return DS2CTC_STATUS_MEMOPS_FAILED;
   for (int c = 1; c < nc; ++c)
@@ -686,19 +719,22 @@ ds2ctc_status ds2ctc_compute_loss_host(const float* activations, float* gradient
     const int bc = b0[c + 1] - b0[c];
     const size_t w = static_cast<size_t>(bc) * A * sizeof(float);
     auto* xd = static_cast<unsigned char*>(ctx.acts) + x_off[c];
-    auto* gd = gradients ? static_cast<unsigned char*>(ctx.grads) + x_off[c] : nullptr;
+    const size_t xpitch = direct ? row : w;
+    auto* gd = !gradients ? nullptr
+               : direct   ? reinterpret_cast<unsigned char*>(g_direct) + x_off[c]
+                          : static_cast<unsigned char*>(ctx.grads) + x_off[c];
     const auto* xh = reinterpret_cast<const unsigned char*>(activations) + static_cast<size_t>(b0[c]) * A * sizeof(float);
     if (t_c[c] > 0 && w > 0 &&
-        cudaMemcpy2DAsync(xd, w, xh, row, w, t_c[c], cudaMemcpyHostToDevice, sc) != cudaSuccess)
+        cudaMemcpy2DAsync(xd, xpitch, xh, row, w, t_c[c], cudaMemcpyHostToDevice, sc) != cudaSuccess)
       return DS2CTC_STATUS_MEMOPS_FAILED;
     float* cd = static_cast<float*>(ctx.costs) + b0[c];
     st = run(reinterpret_cast<const float*>(xd), reinterpret_cast<float*>(gd), flat_labels + lab0[c],
              label_lengths + b0[c], input_lengths + b0[c], A, bc, blank_label, cd,
-             static_cast<unsigned char*>(ctx.ws) + ws_off[c], ws_off[c + 1] - ws_off[c], true, sc);
+             static_cast<unsigned char*>(ctx.ws) + ws_off[c], ws_off[c + 1] - ws_off[c], true, sc, direct ? B : 0);
     if (st != DS2CTC_STATUS_SUCCESS) return st;
     if (gradients && t_c[c] > 0 && w > 0) {
       auto* gh = reinterpret_cast<unsigned char*>(gradients) + static_cast<size_t>(b0[c]) * A * sizeof(float);
-      if (cudaMemcpy2DAsync(gh, row, gd, w, w, t_c[c], cudaMemcpyDeviceToHost, sc) != cudaSuccess)
+      if (!direct && cudaMemcpy2DAsync(gh, row, gd, w, w, t_c[c], cudaMemcpyDeviceToHost, sc) != cudaSuccess)
         return DS2CTC_STATUS_MEMOPS_FAILED;
       // frames past this chunk's longest utterance: zero rows (the contract), on the host
       for (int t = t_c[c]; t < lay.t_max; ++t) std::memset(gh + static_cast<size_t>(t) * row, 0, w);

@@ -283,7 +283,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   const int NCW = g.nchain;
   const bool want_grad = a.grad != nullptr;
   const bool fused = g.fused != 0;
-  const size_t rs = static_cast<size_t>(a.B) * a.A;  // frame stride of [T][B][A]
+  const size_t rs = static_cast<size_t>(a.ld) * a.A;  // frame stride of [T][ld][A]
 
   auto zero_rows = [&](int lo, int hi) {
     for (int t = lo; t < hi; ++t) {

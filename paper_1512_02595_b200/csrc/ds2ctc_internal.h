@@ -213,6 +213,7 @@ struct PairArgs {
   double* logz;          // [B] log2-domain log Z (-inf when the lattice has zero mass)
   double* part;          // [2B] per-CTA partial sums of lse (fused path)
   int t_max, B, A, blank;
+  int ld;  // frame stride of x / grad in utterances (B, or the caller's batch for a sub-batch view)
   Geometry g;
 };
 

@@ -196,6 +196,28 @@ def test_host_api_chunked_ragged_vs_oracle(cuda):
     assert_parity(costs.astype(np.float64), grads, rc, rg, il, "host-chunked")
     c2, _ = dctc.compute_ctc_loss_host(acts, flat, ll, il, want_grad=False)
     assert_parity(c2.astype(np.float64), None, rc, None, il, "host-chunked-cost-only")
+    # page-locked gradient buffer (under DS2CTC_HOST_DIRECT=1, k_pair writes the
+    # rows straight into it; test_host_api_direct_mode reruns this test so)
+    import torch
+
+    pinned = torch.full(acts.shape, float("nan"), dtype=torch.float32).pin_memory()
+    c3, g3 = dctc.compute_ctc_loss_host(acts, flat, ll, il, gradients=pinned.numpy())
+    assert_parity(c3.astype(np.float64), g3, rc, rg, il, "host-direct")
+    assert np.array_equal(g3, grads) and np.array_equal(c3, costs)
+
+
+def test_host_api_direct_mode(cuda):
+    # the opt-in direct-to-host gradient mode is read once per process: rerun
+    # the chunked host test in a child process with it switched on
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, DS2CTC_HOST_DIRECT="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        f"{__file__}::test_host_api_chunked_ragged_vs_oracle"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 
 def test_fused_loss_allreduce_single_rank(cuda):
