@@ -93,6 +93,7 @@ struct Profiler {
     return calls < slots;
   }
   void mark(int i, cudaStream_t s) { cudaEventRecord(ev[4 * calls + i], s); }
+  bool suspended = false;  // inside a length-split call: one record for the whole call
 };
 
 Profiler& profiler() {
@@ -296,7 +297,7 @@ ds2ctc_status run(const float* acts, float* grads, const int* flat_labels, const
   int dev = 0;
   cudaGetDevice(&dev);
   Profiler& prof = profiler();
-  const bool timed = prof.ready(dev);
+  const bool timed = !prof.suspended && prof.ready(dev);
   if (timed) prof.mark(0, s);
   if (launch_pair(a, stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
   if (timed) prof.mark(1, s);
@@ -496,6 +497,134 @@ const char* ds2ctc_status_string(ds2ctc_status status) {
 
 const char* ds2ctc_version(void) { return "ds2ctc 0.1.0 sm_100a"; }
 
+// Length-split device call. A variable-length batch (SortaGrad) runs as up to
+// four contiguous sub-batches, each launched with the geometry of its own
+// longest label (fewer chain warps, less shared memory, more CTAs per SM for
+// the short ones) on forked streams that join back into the caller's stream.
+// Split only when some quarter's longest label is under 3/4 of the batch's,
+// so fixed-shape batches keep the single launch. Fused path only (A <= 128):
+// the sub-batch views use frame stride B.
+constexpr int kDevSplitMax = 4;
+
+struct SplitPlan {
+  int n = 1;
+  int b0[kDevSplitMax + 1];
+  size_t lab0[kDevSplitMax];
+  size_t ws_off[kDevSplitMax + 1];
+};
+
+bool dev_split_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("DS2CTC_LENGTH_SPLIT");
+    return v == nullptr || std::atoi(v) != 0;
+  }();
+  return on;
+}
+
+SplitPlan plan_split(const int* label_lengths, const int* input_lengths, int A, int B) {
+  SplitPlan p;
+  p.b0[0] = 0;
+  p.b0[1] = B;
+  p.lab0[0] = 0;
+  p.ws_off[0] = 0;
+  if (B >= 64 && A <= kFusedMaxAlphabet && dev_split_enabled()) {
+    int lmax_all = 0, lmax_min = 1 << 30;
+    for (int c = 0; c < kDevSplitMax; ++c) {
+      int m = 0;
+      for (int b = B * c / kDevSplitMax; b < B * (c + 1) / kDevSplitMax; ++b) m = std::max(m, label_lengths[b]);
+      lmax_all = std::max(lmax_all, m);
+      lmax_min = std::min(lmax_min, m);
+    }
+    if (4LL * lmax_min < 3LL * lmax_all) p.n = kDevSplitMax;
+  }
+  size_t lab = 0;
+  for (int c = 0; c < p.n; ++c) {
+    p.b0[c + 1] = static_cast<int>(static_cast<long long>(B) * (c + 1) / p.n);
+    p.lab0[c] = lab;
+    for (int b = p.b0[c]; b < p.b0[c + 1]; ++b) lab += static_cast<size_t>(label_lengths[b]);
+    const size_t wsz =
+        make_layout(label_lengths + p.b0[c], input_lengths + p.b0[c], A, p.b0[c + 1] - p.b0[c]).total;
+    p.ws_off[c + 1] = p.ws_off[c] + (wsz + kAlign - 1) / kAlign * kAlign;
+  }
+  return p;
+}
+
+struct SplitStreams {
+  cudaStream_t s[kDevSplitMax - 1] = {};
+  cudaEvent_t fork = nullptr;
+  cudaEvent_t join[kDevSplitMax - 1] = {};
+  bool init() {
+    if (fork) return true;
+    for (auto& x : s)
+      if (cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking) != cudaSuccess) return false;
+    for (auto& e : join)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return false;
+    return cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) == cudaSuccess;
+  }
+};
+
+ds2ctc_status run_split(const float* acts, float* grads, const int* flat_labels, const int* label_lengths,
+                        const int* input_lengths, int A, int B, int blank, float* costs, void* workspace,
+                        size_t workspace_bytes, bool check_ws, void* stream) {
+  ds2ctc_status st = validate(label_lengths, input_lengths, A, B, blank, flat_labels);
+  if (st != DS2CTC_STATUS_SUCCESS || B == 0) return st;
+  const SplitPlan p = plan_split(label_lengths, input_lengths, A, B);
+  if (p.n == 1)
+    return run(acts, grads, flat_labels, label_lengths, input_lengths, A, B, blank, costs, workspace,
+               workspace_bytes, check_ws, stream);
+  if (check_ws && workspace_bytes < p.ws_off[p.n]) return DS2CTC_STATUS_INVALID_VALUE;
+  if (costs == nullptr || workspace == nullptr) return DS2CTC_STATUS_INVALID_VALUE;
+  thread_local std::map<int, SplitStreams> per_device;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SplitStreams& ss = per_device[dev];
+  if (!ss.init()) return DS2CTC_STATUS_EXECUTION_FAILED;
+  auto s0 = static_cast<cudaStream_t>(stream);
+  // stage events (ds2ctc_profile_*): k_pair = fork to join of the whole call
+  Profiler& prof = profiler();
+  const bool timed = prof.ready(dev);
+  if (timed) prof.mark(0, s0);
+  struct Suspend {
+    Profiler& p;
+    ~Suspend() { p.suspended = false; }
+  } suspend{prof};
+  prof.suspended = true;
+  if (cudaEventRecord(ss.fork, s0) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  for (int c = 1; c < p.n; ++c)
+    if (cudaStreamWaitEvent(ss.s[c - 1], ss.fork, 0) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  int t_max = 0;
+  for (int b = 0; b < B; ++b) t_max = std::max(t_max, input_lengths[b]);
+  for (int c = 0; c < p.n; ++c) {
+    const size_t col = static_cast<size_t>(p.b0[c]) * A;
+    // each launch zero-fills padded rows only up to its own longest utterance:
+    // the rest of this chunk's columns, up to the batch's T_max, here
+    int t_c = 0;
+    for (int b = p.b0[c]; b < p.b0[c + 1]; ++b) t_c = std::max(t_c, input_lengths[b]);
+    const size_t pitch = static_cast<size_t>(B) * A * sizeof(float);
+    if (grads && t_c < t_max &&
+        cudaMemset2DAsync(grads + static_cast<size_t>(t_c) * B * A + col, pitch, 0,
+                          static_cast<size_t>(p.b0[c + 1] - p.b0[c]) * A * sizeof(float), t_max - t_c,
+                          c == 0 ? s0 : ss.s[c - 1]) != cudaSuccess)
+      return DS2CTC_STATUS_EXECUTION_FAILED;
+    st = run(acts + col, grads ? grads + col : nullptr, flat_labels + p.lab0[c], label_lengths + p.b0[c],
+             input_lengths + p.b0[c], A, p.b0[c + 1] - p.b0[c], blank, costs + p.b0[c],
+             static_cast<unsigned char*>(workspace) + p.ws_off[c], p.ws_off[c + 1] - p.ws_off[c], true,
+             c == 0 ? stream : ss.s[c - 1], B);
+    if (st != DS2CTC_STATUS_SUCCESS) return st;
+  }
+  for (int c = 1; c < p.n; ++c)
+    if (cudaEventRecord(ss.join[c - 1], ss.s[c - 1]) != cudaSuccess ||
+        cudaStreamWaitEvent(s0, ss.join[c - 1], 0) != cudaSuccess)
+      return DS2CTC_STATUS_EXECUTION_FAILED;
+  if (timed) {
+    prof.mark(1, s0);
+    prof.mark(2, s0);
+    prof.mark(3, s0);
+    ++prof.calls;
+  }
+  return DS2CTC_STATUS_SUCCESS;
+}
+
 ds2ctc_status ds2ctc_get_workspace_size(const int* label_lengths, const int* input_lengths, int alphabet_size,
                                         int minibatch, size_t* bytes) {
   if (bytes == nullptr || minibatch < 0 || alphabet_size < 2) return DS2CTC_STATUS_INVALID_VALUE;
@@ -504,23 +633,27 @@ ds2ctc_status ds2ctc_get_workspace_size(const int* label_lengths, const int* inp
     if (label_lengths[b] < 0 || input_lengths[b] < 0) return DS2CTC_STATUS_INVALID_VALUE;
     if (2LL * label_lengths[b] + 1 > kMaxStates) return DS2CTC_STATUS_UNSUPPORTED;
   }
-  *bytes = minibatch == 0 ? 0 : make_layout(label_lengths, input_lengths, alphabet_size, minibatch).total;
+  *bytes = 0;
+  if (minibatch > 0) {
+    const SplitPlan p = plan_split(label_lengths, input_lengths, alphabet_size, minibatch);
+    *bytes = p.n == 1 ? make_layout(label_lengths, input_lengths, alphabet_size, minibatch).total : p.ws_off[p.n];
+  }
   return DS2CTC_STATUS_SUCCESS;
 }
 
 ds2ctc_status ds2ctc_compute_loss(const float* activations, float* gradients, const int* flat_labels,
                                   const int* label_lengths, const int* input_lengths, int alphabet_size,
                                   int minibatch, int blank_label, float* costs, void* workspace, void* stream) {
-  return run(activations, gradients, flat_labels, label_lengths, input_lengths, alphabet_size, minibatch,
-             blank_label, costs, workspace, 0, false, stream);
+  return run_split(activations, gradients, flat_labels, label_lengths, input_lengths, alphabet_size, minibatch,
+                   blank_label, costs, workspace, 0, false, stream);
 }
 
 ds2ctc_status ds2ctc_compute_loss_checked(const float* activations, float* gradients, const int* flat_labels,
                                           const int* label_lengths, const int* input_lengths, int alphabet_size,
                                           int minibatch, int blank_label, float* costs, void* workspace,
                                           size_t workspace_bytes, void* stream) {
-  return run(activations, gradients, flat_labels, label_lengths, input_lengths, alphabet_size, minibatch,
-             blank_label, costs, workspace, workspace_bytes, true, stream);
+  return run_split(activations, gradients, flat_labels, label_lengths, input_lengths, alphabet_size, minibatch,
+                   blank_label, costs, workspace, workspace_bytes, true, stream);
 }
 
 ds2ctc_status ds2ctc_viterbi_get_workspace_size(const int* label_lengths, const int* input_lengths,
