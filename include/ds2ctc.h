@@ -83,6 +83,11 @@ ds2ctc_status ds2ctc_get_workspace_size(const int* label_lengths, const int* inp
  *   costs         DEVICE fp32 [minibatch] (-log p, +inf when infeasible).
  *   workspace     DEVICE, at least ds2ctc_get_workspace_size() bytes, 256-byte aligned.
  *   stream        cudaStream_t (NULL = legacy default stream). Asynchronous.
+ *                 A variable-length batch (B >= 64, alphabet <= 128, labels
+ *                 spread by length) may run as length-split sub-batches on
+ *                 library streams forked from and joined back into `stream`
+ *                 (DS2CTC_LENGTH_SPLIT=0 disables); ordering w.r.t. `stream`
+ *                 is unchanged, and the workspace query accounts for it.
  * minibatch == 0 is a valid no-op (an empty data-parallel shard, trainer.cpp:141-155).
  */
 ds2ctc_status ds2ctc_compute_loss(const float* activations, float* gradients, const int* flat_labels,

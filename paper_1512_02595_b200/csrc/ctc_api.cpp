@@ -504,7 +504,7 @@ const char* ds2ctc_version(void) { return "ds2ctc 0.1.0 sm_100a"; }
 // Split only when some quarter's longest label is under 3/4 of the batch's,
 // so fixed-shape batches keep the single launch. Fused path only (A <= 128):
 // the sub-batch views use frame stride B.
-constexpr int kDevSplitMax = 4;
+constexpr int kDevSplitMax = 8;
 
 struct SplitPlan {
   int n = 1;
@@ -513,12 +513,15 @@ struct SplitPlan {
   size_t ws_off[kDevSplitMax + 1];
 };
 
-bool dev_split_enabled() {
-  static const bool on = [] {
+// DS2CTC_LENGTH_SPLIT: 0 = single launch, n >= 2 = n sub-batches; default
+// 8 from B = 128 up, else 4 (SortaGrad B = 512: 8 -> 303k, 4 -> 298k utt/s)
+int dev_split_count(int B) {
+  static const int n = [] {
     const char* v = std::getenv("DS2CTC_LENGTH_SPLIT");
-    return v == nullptr || std::atoi(v) != 0;
+    const int k = v ? std::atoi(v) : -1;
+    return k < 0 ? -1 : k <= 1 ? 1 : std::min(k, kDevSplitMax);
   }();
-  return on;
+  return n > 0 ? n : (B >= 128 ? 8 : 4);
 }
 
 SplitPlan plan_split(const int* label_lengths, const int* input_lengths, int A, int B) {
@@ -527,15 +530,16 @@ SplitPlan plan_split(const int* label_lengths, const int* input_lengths, int A, 
   p.b0[1] = B;
   p.lab0[0] = 0;
   p.ws_off[0] = 0;
-  if (B >= 64 && A <= kFusedMaxAlphabet && dev_split_enabled()) {
+  const int ns = dev_split_count(B);
+  if (B >= 16 * ns && ns > 1 && A <= kFusedMaxAlphabet) {
     int lmax_all = 0, lmax_min = 1 << 30;
-    for (int c = 0; c < kDevSplitMax; ++c) {
+    for (int c = 0; c < ns; ++c) {
       int m = 0;
-      for (int b = B * c / kDevSplitMax; b < B * (c + 1) / kDevSplitMax; ++b) m = std::max(m, label_lengths[b]);
+      for (int b = B * c / ns; b < B * (c + 1) / ns; ++b) m = std::max(m, label_lengths[b]);
       lmax_all = std::max(lmax_all, m);
       lmax_min = std::min(lmax_min, m);
     }
-    if (4LL * lmax_min < 3LL * lmax_all) p.n = kDevSplitMax;
+    if (4LL * lmax_min < 3LL * lmax_all) p.n = ns;
   }
   size_t lab = 0;
   for (int c = 0; c < p.n; ++c) {

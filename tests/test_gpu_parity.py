@@ -114,14 +114,15 @@ def test_sortagrad_variable_vs_oracle(cuda):
 def test_sortagrad_sorted_length_split_vs_oracle(cuda):
     # a SortaGrad (epoch 0) minibatch sorted by length, B >= 64: the device call
     # runs as four length-split sub-batch launches on forked streams
-    T, L = sortagrad_lengths(96, seed=13)
-    order = np.argsort(T, kind="stable")
-    acts, flat, ll, il = make_batch(29, T[order], L[order], seed=6)
-    costs, grads = run_gpu(acts, flat, ll, il)
-    rc, rg = oracle.oracle_batch(acts, flat, ll, il, nthreads=8)
-    assert_parity(costs, grads, rc, rg, il, "sortagrad-split")
-    c2, g2 = run_gpu(acts, flat, ll, il)
-    assert np.array_equal(c2, costs) and np.array_equal(g2, grads)
+    for n, seed in ((96, 13), (256, 14)):  # 4-way and 8-way splits
+        T, L = sortagrad_lengths(n, seed=seed)
+        order = np.argsort(T, kind="stable")
+        acts, flat, ll, il = make_batch(29, T[order], L[order], seed=6)
+        costs, grads = run_gpu(acts, flat, ll, il)
+        rc, rg = oracle.oracle_batch(acts, flat, ll, il, nthreads=8)
+        assert_parity(costs, grads, rc, rg, il, f"sortagrad-split-{n}")
+        c2, g2 = run_gpu(acts, flat, ll, il)
+        assert np.array_equal(c2, costs) and np.array_equal(g2, grads)
 
 
 @pytest.mark.parametrize("A,T,L,B", [(29, 1300, 600, 2), (29, 2100, 1000, 2), (200, 300, 90, 4), (5, 40, 15, 33)])
