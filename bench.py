@@ -181,11 +181,31 @@ def run_reference(args, wl):
                                    f"asr::ctc::ctc_loss_reference fp64, one utterance per thread"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    emit(line)
     return 0
 
 
+# The contract is ONE JSON line on stdout; native libraries (NCCL's
+# "NCCL version" banner at communicator init) print to fd 1 directly, so fd 1
+# is pointed at stderr and the JSON line goes to a saved copy of the original.
+_JSON_OUT = None
+
+
+def claim_stdout() -> None:
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w", buffering=1)
+    os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    claim_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
@@ -436,7 +456,7 @@ def main():
                                     "sample": f"{done} utterances ({n} per batch) of the {args.workload} "
                                               f"workload in {el:.1f} s, asr::ctc::ctc_loss_reference fp64, "
                                               f"one utterance per thread"}
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.barrier()
         if peer is not None:

@@ -83,7 +83,7 @@ ds2ctc_status ds2ctc_get_workspace_size(const int* label_lengths, const int* inp
  *   costs         DEVICE fp32 [minibatch] (-log p, +inf when infeasible).
  *   workspace     DEVICE, at least ds2ctc_get_workspace_size() bytes, 256-byte aligned.
  *   stream        cudaStream_t (NULL = legacy default stream). Asynchronous.
- *                 A variable-length batch (B >= 64, alphabet <= 128, labels
+ *                 A variable-length batch (B >= 256, alphabet <= 128, labels
  *                 spread by length) may run as length-split sub-batches on
  *                 library streams forked from and joined back into `stream`
  *                 (DS2CTC_LENGTH_SPLIT=0 disables); ordering w.r.t. `stream`

@@ -514,14 +514,17 @@ struct SplitPlan {
 };
 
 // DS2CTC_LENGTH_SPLIT: 0 = single launch, n >= 2 = n sub-batches; default
-// 8 from B = 128 up, else 4 (SortaGrad B = 512: 8 -> 303k, 4 -> 298k utt/s)
+// 8 from B = 256 up, else none. Measured SortaGrad: B = 512 (1 GPU) 230k ->
+// 298k (4) / 303k (8) utt/s; B = 256 per GPU (2 GPUs) 428k -> 506k (8);
+// B = 128 per GPU (4 GPUs) 780k (none) vs 773k (4) / 720k (8): one wave of
+// clusters already holds the whole batch there.
 int dev_split_count(int B) {
   static const int n = [] {
     const char* v = std::getenv("DS2CTC_LENGTH_SPLIT");
     const int k = v ? std::atoi(v) : -1;
     return k < 0 ? -1 : k <= 1 ? 1 : std::min(k, kDevSplitMax);
   }();
-  return n > 0 ? n : (B >= 128 ? 8 : 4);
+  return n > 0 ? n : (B >= 256 ? 8 : 1);
 }
 
 SplitPlan plan_split(const int* label_lengths, const int* input_lengths, int A, int B) {
@@ -531,7 +534,7 @@ SplitPlan plan_split(const int* label_lengths, const int* input_lengths, int A, 
   p.lab0[0] = 0;
   p.ws_off[0] = 0;
   const int ns = dev_split_count(B);
-  if (B >= 16 * ns && ns > 1 && A <= kFusedMaxAlphabet) {
+  if (ns > 1 && B >= 16 * ns && A <= kFusedMaxAlphabet) {
     int lmax_all = 0, lmax_min = 1 << 30;
     for (int c = 0; c < ns; ++c) {
       int m = 0;

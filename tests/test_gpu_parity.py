@@ -112,9 +112,9 @@ def test_sortagrad_variable_vs_oracle(cuda):
 
 
 def test_sortagrad_sorted_length_split_vs_oracle(cuda):
-    # a SortaGrad (epoch 0) minibatch sorted by length, B >= 64: the device call
-    # runs as four length-split sub-batch launches on forked streams
-    for n, seed in ((96, 13), (256, 14)):  # 4-way and 8-way splits
+    # a SortaGrad (epoch 0) minibatch sorted by length, B >= 256: the device
+    # call runs as eight length-split sub-batch launches on forked streams
+    for n, seed in ((256, 14), (320, 13)):  # 8-way splits (B >= 256)
         T, L = sortagrad_lengths(n, seed=seed)
         order = np.argsort(T, kind="stable")
         acts, flat, ll, il = make_batch(29, T[order], L[order], seed=6)
