@@ -56,6 +56,15 @@ WORKLOADS = {
 }
 
 
+def bench_config(name: str, wl: dict, n_gpus: int) -> dict:
+    """The workload description both arms print as `config` (identical dicts, so
+    the driver can match the arms); arm-specific details go outside it."""
+    il_g, ll_g = global_batch(wl, n_gpus)
+    return {"workload": name, "desc": wl["desc"], "alphabet": wl["A"], "global_batch": int(il_g.shape[0]),
+            "frames_per_step": int(il_g.sum()), "labels_per_step": int(ll_g.sum()),
+            "parallelism": f"dp{n_gpus}", "l2": "flushed between steps (256 MiB memset)"}
+
+
 def global_batch(wl: dict, n_gpus: int, seed: int = 1234):
     """(input_lengths, label_lengths) of the global minibatch."""
     if "per_gpu" in wl:
@@ -130,7 +139,9 @@ class ClockSampler:
 
 
 def cpu_reference_rate(acts, flat, ll, il, nthreads, min_seconds):
-    """The reference's own ctc_loss_reference (oracle/_ref build) on host cores; utt/s."""
+    """The reference's own ctc_loss_reference (oracle/_ref build) on host cores; utt/s.
+    Also returns the last call's (costs, grads): the reference's answer on these
+    inputs, which the parity gate compares with the GPU's."""
     import oracle
 
     kind = "reference" if oracle.ref_available() else "port"
@@ -139,12 +150,33 @@ def cpu_reference_rate(acts, flat, ll, il, nthreads, min_seconds):
     done = 0
     t0 = time.perf_counter()
     while True:
-        fn(acts, flat, ll, il, nthreads=nthreads)
+        out = fn(acts, flat, ll, il, nthreads=nthreads)
         done += ll.shape[0]
         el = time.perf_counter() - t0
         if el >= min_seconds:
             break
-    return done / el, kind, done, el
+    return done / el, kind, done, el, out
+
+
+def parity_gate(costs, grads, ref_costs, ref_grads, il):
+    """SURVEY.md §8(d) same-run parity gate: per utterance |cost - ref| / |ref| <= 1e-4,
+    max |grad - ref| <= 1e-4; infeasible -> +inf and all-zero rows (NaN patterns must match)."""
+    costs = np.asarray(costs, np.float64)
+    ref_costs = np.asarray(ref_costs, np.float64)
+    inf_ok = bool(np.array_equal(np.isposinf(costs), np.isposinf(ref_costs)))
+    nan_ok = bool(np.array_equal(np.isnan(costs), np.isnan(ref_costs)))
+    fin = np.isfinite(ref_costs)
+    rel = float((np.abs(costs[fin] - ref_costs[fin]) / np.maximum(np.abs(ref_costs[fin]), 1e-30)).max()) \
+        if fin.any() else 0.0
+    g = np.asarray(grads, np.float64)
+    r = np.asarray(ref_grads, np.float64)
+    gnan_ok = bool(np.array_equal(np.isnan(g), np.isnan(r)))
+    gerr = float(np.nanmax(np.abs(g - r))) if g.size else 0.0
+    for b in np.where(np.isposinf(ref_costs))[0]:
+        inf_ok = inf_ok and bool(np.all(g[:, b, :] == 0))
+    ok = inf_ok and nan_ok and gnan_ok and rel <= 1e-4 and gerr <= 1e-4
+    return {"utterances": int(costs.shape[0]), "max_rel_cost": rel, "max_abs_grad": gerr,
+            "tolerance": {"rel_cost": 1e-4, "abs_grad": 1e-4}, "ok": ok}
 
 
 def run_reference(args, wl):
@@ -154,7 +186,7 @@ def run_reference(args, wl):
         return 0
     import oracle
 
-    il_g, ll_g = global_batch(wl, 1)
+    il_g, ll_g = global_batch(wl, args.gpus)
     n = min(64, il_g.shape[0])
     acts, flat, ll, il = shard_inputs(wl, il_g, ll_g, np.arange(n), 0)
     nthreads = os.cpu_count() or 1
@@ -173,8 +205,9 @@ def run_reference(args, wl):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": wl["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "desc": wl["desc"], "utterances_per_step": n,
-                   "frames_per_step": int(il.sum())},
+        "config": bench_config(args.workload, wl, args.gpus),
+        "sample": {"utterances_per_step": n, "frames_per_step": int(il.sum()),
+                   "note": "each step is a bounded sample of the workload's global batch (the first n utterances)"},
         "frames_per_s": float(il.sum()) / (ms / 1e3),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": kind,
                          "sample": f"{n} utterances of the {args.workload} workload per step, "
@@ -390,14 +423,24 @@ def main():
         alg_bytes = 8.0 * float((il.astype(np.float64) * A).sum()) + 4.0 * float(ll.sum()) + 8.0 * B
         dom_name, dom_ms = ("k_pair", pair_ms) if pair_ms >= dense_ms else ("k_dense", dense_ms)
         achieved = alg_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
-        traffic = None
+        # DRAM bytes per launch of the dominant kernel from one `ncu --set full`
+        # capture (tools/ncu/traffic.py), valid only for the exact library it was
+        # measured on: profiles/ncu_traffic.json is stamped with the content hash
+        # of the sources the library was built from (libds2ctc.so.sha256).
+        traffic, traffic_src = None, "no capture for this build"
         tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tpath):
-            try:
-                with open(tpath) as f:
-                    traffic = json.load(f).get(args.workload)
-            except Exception:
-                traffic = None
+        try:
+            with open(tpath) as f:
+                tj = json.load(f)
+            with open(_lib.LIB_PATH + ".sha256") as f:
+                lib_hash = f.read().strip()
+            if tj.get("lib_sha256") == lib_hash and args.workload in tj.get("bytes", {}):
+                traffic = float(tj["bytes"][args.workload])
+                traffic_src = f"profiles/ncu_traffic.json ({tj.get('kernel', dom_name)}, build {lib_hash[:12]})"
+            else:
+                traffic_src = "profiles/ncu_traffic.json is from another build (source hash mismatch)"
+        except Exception as exc:  # noqa: BLE001
+            traffic_src = f"unavailable ({type(exc).__name__})"
         # The binding bound at small alphabets is the serial lattice chain, not HBM
         # (DESIGN.md §5.1): each CTA of k_pair runs T_max dependent steps. Report the
         # measured cycles per step beside the isolated-step floor measured by
@@ -430,16 +473,15 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": wl["scaling"],
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": args.workload, "desc": wl["desc"], "alphabet": A,
-                       "global_batch": total_utts, "frames_per_step": total_frames,
-                       "parallelism": f"dp{world}", "l2": "flushed between steps (256 MiB memset)",
-                       "scalar_reduce": ("nvlink peer mailboxes (ds2ctc_loss_sum_allreduce)" if peer is not None
-                                         else ("nccl all_reduce" if world > 1 else "none"))},
+            "config": bench_config(args.workload, wl, world),
+            "scalar_reduce": ("nvlink peer mailboxes (ds2ctc_loss_sum_allreduce)" if peer is not None
+                              else ("nccl all_reduce" if world > 1 else "none")),
             "frames_per_s": total_frames / (ms / 1e3),
             "stage_ms": {"k_pair": pair_ms, "k_dense": dense_ms, "k_finalize": final_ms},
             "roofline": {"bound": "hbm", "kernel": dom_name, "kernel_ms": dom_ms, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "alg_bytes_per_launch": alg_bytes, "chain": chain},
+                         "traffic": traffic, "traffic_source": traffic_src, "alg_bytes_per_launch": alg_bytes,
+                         "chain": chain},
             "e2e": {"value": total_utts / (e2e_ms / 1e3), "unit": UNIT,
                     "h2d_bytes_per_step": int(acts_h.nbytes + 4 * (ll.sum() + 2 * B)),
                     "d2h_bytes_per_step": int(acts_h.nbytes + 4 * B), "ms_per_step": e2e_ms},
@@ -448,14 +490,31 @@ def main():
             "loss_sum": loss_sum, "skipped": int(skipped),
         }
         if world == 1 and not args.no_cpu_baseline:
+            # The reference CPU CTC on the same inputs: (i) all host cores, one
+            # utterance per thread (the paper's CPU CTC); (ii) one
+            # core, the trainer's serial loop (trainer.cpp:158-169). Its answers
+            # on the sample are the same-run parity gate for the GPU's.
             n = min(64, B)
             sub = np.arange(n)
-            rate, kind, done, el = cpu_reference_rate(acts_h[:, sub, :], flat[:int(ll[:n].sum())], ll[:n], il[:n],
-                                                      os.cpu_count() or 1, args.cpu_seconds)
+            nl = int(ll[:n].sum())
+            t_n = int(il[:n].max()) if n else 0
+            rate, kind, done, el, (rc, rg) = cpu_reference_rate(
+                np.ascontiguousarray(acts_h[:t_n, sub, :]), flat[:nl], ll[:n], il[:n], os.cpu_count() or 1,
+                args.cpu_seconds)
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": kind,
                                     "sample": f"{done} utterances ({n} per batch) of the {args.workload} "
                                               f"workload in {el:.1f} s, asr::ctc::ctc_loss_reference fp64, "
                                               f"one utterance per thread"}
+            n1 = min(8, n)
+            rate1, kind1, done1, el1, _ = cpu_reference_rate(
+                np.ascontiguousarray(acts_h[:int(il[:n1].max()), :n1, :]), flat[:int(ll[:n1].sum())], ll[:n1],
+                il[:n1], 1, args.cpu_seconds / 2)
+            line["cpu_baseline_serial"] = {"value": rate1, "unit": UNIT, "cores": 1, "kind": kind1,
+                                           "sample": f"{done1} utterances ({n1} per batch) in {el1:.1f} s, one "
+                                                     f"core, serial as train_epoch calls it (trainer.cpp:158-169)"}
+            g_host = grads.cpu().numpy()[:t_n, :n, :] if B else np.zeros((0, 0, A), np.float32)
+            line["parity"] = parity_gate(costs.cpu().numpy()[:n], g_host, rc, rg, il[:n])
+            line["parity"]["checker"] = f"{kind} ({'oracle/_ref build of ctc_loss_reference' if kind == 'reference' else 'oracle port'}), first {n} utterances of the timed batch"
         emit(line)
     if world > 1:
         dist.barrier()

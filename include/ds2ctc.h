@@ -170,6 +170,8 @@ ds2ctc_status ds2ctc_ctc_lattice_host(const float* activations, const int* flat_
 
 /*
  * Per-shard {sum of feasible costs, number of infeasible utterances} as fp64
+ * (infeasible = cost +inf; a NaN cost is feasible, as in the reference, and
+ * makes the sum NaN)
  * [2] on the device, the two scalars train_epoch accumulates
  * (local_loss / local_skipped, trainer.cpp:160-168) and all-reduces
  * (trainer.cpp:176-179). Fixed summation order (deterministic). costs and
@@ -195,6 +197,15 @@ ds2ctc_status ds2ctc_mailbox_open(const void* ipc_handle, void** peer_mailbox);
 ds2ctc_status ds2ctc_mailbox_close(void* peer_mailbox, int own);
 ds2ctc_status ds2ctc_loss_sum_allreduce(const float* costs, int minibatch, double* out2, void* const* peer_mailboxes,
                                         int rank, int world, unsigned long long seq, void* stream);
+/*
+ * Lost-peer check of ds2ctc_loss_sum_allreduce. Each call waits at most 20 s
+ * (%globaltimer) for the peers' pairs of its step; on timeout it writes NaN
+ * into out2 (never a stale fold) and records the step. This reads (after
+ * the recorded kernels finished: it synchronises with the device's legacy
+ * stream) and clears the first timed-out `seq`, 0 if none. After a timeout
+ * the mailboxes must be closed and re-created on every rank.
+ */
+ds2ctc_status ds2ctc_reduce_fault(unsigned long long* seq);
 
 /*
  * Stage timing for benchmarks: when enabled for the calling thread with

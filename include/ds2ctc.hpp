@@ -27,6 +27,7 @@
 #include <limits>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "ds2ctc.h"
@@ -38,6 +39,20 @@ struct CtcResult {
   bool feasible = false;
   double loss = std::numeric_limits<double>::infinity();
   M logit_grad;  // T x A; empty when infeasible
+
+  // Converts to any result type with the reference's fields, so a caller
+  // that spells the type out keeps compiling after the one-identifier switch:
+  //   asr::ctc::CtcResult res = ds2ctc::ctc_loss_gpu(logits, label, blank);
+  // (asr::ctc::CtcResult, ctc.hpp:62-66: feasible, loss, logit_grad)
+  template <class R, class = decltype(std::declval<R&>().feasible = true, std::declval<R&>().loss = 0.0,
+                                      std::declval<R&>().logit_grad = std::declval<const M&>())>
+  operator R() const {
+    R r;
+    r.feasible = feasible;
+    r.loss = static_cast<decltype(r.loss)>(loss);
+    r.logit_grad = logit_grad;
+    return r;
+  }
 };
 
 inline void check(ds2ctc_status st, const char* where) {
@@ -57,7 +72,7 @@ CtcResult<M> ctc_loss_gpu(const M& frame_logits, const std::vector<int>& label, 
   check(ds2ctc_compute_loss_host(x.data(), g.data(), label.data(), &L, &T, A, 1, blank, &cost, device),
         "ctc_loss_gpu");
   CtcResult<M> res;
-  if (!std::isfinite(cost)) return res;
+  if (std::isinf(cost) && cost > 0) return res;  // infeasible (ctc.cpp:173,189-193); NaN stays feasible
   res.feasible = true;
   res.loss = cost;
   res.logit_grad = M(T, A);
@@ -130,6 +145,19 @@ struct CtcLattice {
   M alpha;  // (2L+1) x T
   M beta;   // (2L+1) x T, emission-exclusive
   double log_prob = -std::numeric_limits<double>::infinity();
+
+  // To asr::ctc::CtcLattice (ctc.hpp:55-60) or any type with these fields.
+  template <class R, class = decltype(std::declval<R&>().augmented_label = std::vector<int>(),
+                                      std::declval<R&>().alpha = std::declval<const M&>(),
+                                      std::declval<R&>().log_prob = 0.0)>
+  operator R() const {
+    R r;
+    r.augmented_label = augmented_label;
+    r.alpha = alpha;
+    r.beta = beta;
+    r.log_prob = static_cast<decltype(r.log_prob)>(log_prob);
+    return r;
+  }
 };
 
 template <class M>

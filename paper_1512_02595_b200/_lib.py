@@ -35,6 +35,7 @@ EXPORTS = (
     "ds2ctc_mailbox_open",
     "ds2ctc_mailbox_close",
     "ds2ctc_loss_sum_allreduce",
+    "ds2ctc_reduce_fault",
     "ds2ctc_viterbi_get_workspace_size",
     "ds2ctc_viterbi_align",
     "ds2ctc_lattice_get_sizes",
@@ -66,6 +67,14 @@ _dp = ctypes.POINTER(ctypes.c_double)
 _szp = ctypes.POINTER(ctypes.c_size_t)
 
 
+class _missing:
+    def __init__(self, name):
+        self.name = name
+
+    def __call__(self, *a):
+        raise RuntimeError(f"{LIB_PATH} (DS2CTC_LIB variant) does not export {self.name}")
+
+
 def lib():
     """Loads the in-tree libds2ctc.so (raises if it was not built)."""
     global _lib
@@ -77,6 +86,14 @@ def lib():
                 raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_1512_02595_b200.build` "
                                   "(there is no CPU fallback)")
             L = ctypes.CDLL(LIB_PATH)
+            if os.environ.get("DS2CTC_LIB"):
+                # a debug variant (e.g. an older build for an A/B) may predate some
+                # entry points: give those a stub that fails loudly if called
+                for name in EXPORTS:
+                    try:
+                        getattr(L, name)
+                    except AttributeError:
+                        setattr(L, name, _missing(name))
             L.ds2ctc_status_string.restype = ctypes.c_char_p
             L.ds2ctc_status_string.argtypes = [ctypes.c_int]
             L.ds2ctc_version.restype = ctypes.c_char_p
@@ -103,6 +120,8 @@ def lib():
             L.ds2ctc_loss_sum_allreduce.restype = ctypes.c_int
             L.ds2ctc_loss_sum_allreduce.argtypes = [_p, ctypes.c_int, _p, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int,
                                                     ctypes.c_int, ctypes.c_ulonglong, _p]
+            L.ds2ctc_reduce_fault.restype = ctypes.c_int
+            L.ds2ctc_reduce_fault.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
             L.ds2ctc_viterbi_get_workspace_size.restype = ctypes.c_int
             L.ds2ctc_viterbi_get_workspace_size.argtypes = [_ip, _ip, ctypes.c_int, ctypes.c_int, _szp]
             L.ds2ctc_lattice_get_sizes.restype = ctypes.c_int
@@ -141,6 +160,13 @@ def watchdog():
     out = (ctypes.c_ulonglong * 4)()
     check(lib().ds2ctc_debug_watchdog(out), "ds2ctc_debug_watchdog")
     return None if out[0] == 0 else tuple(int(v) for v in out)
+
+
+def reduce_fault():
+    """The step (seq) of the first fused all-reduce whose peer wait timed out since the last call, or None."""
+    out = ctypes.c_ulonglong(0)
+    check(lib().ds2ctc_reduce_fault(ctypes.byref(out)), "ds2ctc_reduce_fault")
+    return None if out.value == 0 else int(out.value)
 
 
 def check(status: int, where: str) -> None:

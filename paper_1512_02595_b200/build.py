@@ -8,6 +8,7 @@ dependency and travels to the GPU box as-is.
 """
 from __future__ import annotations
 
+import hashlib
 import os
 import shutil
 import subprocess
@@ -21,7 +22,10 @@ LIB = os.path.join(PKG, "libds2ctc.so")
 BUILD = os.path.join(PKG, "_build")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["ctc_pair.cu", "ctc_dense.cu", "ctc_viterbi.cu", "ctc_lattice.cu", "ctc_reduce.cu"]
+CU_SOURCES = ["ctc_pair.cu", "ctc_pair_k8.cu", "ctc_dense.cu", "ctc_viterbi.cu", "ctc_lattice.cu", "ctc_reduce.cu"]
+# Per-source extra flags. ctc_pair_k8.cu: ptxas 12.9 -O3 segfaults on the
+# K = 8 pair kernel at its 168-register budget; -O1 builds it without spills.
+CU_FLAGS = {"ctc_pair_k8.cu": ["-Xptxas", "-O1"]}
 CPP_SOURCES = ["ctc_api.cpp", "scheduler.cpp"]
 
 
@@ -32,11 +36,29 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def _newer(target: str, deps) -> bool:
-    if not os.path.exists(target):
+def _content_hash(deps, flags) -> str:
+    """sha256 over every source's bytes, the build flags and the compiler version:
+    a prebuilt library is reused only if it was built from exactly these inputs
+    (modification times are not trusted: a snapshot copy can reorder them)."""
+    h = hashlib.sha256()
+    for d in sorted(deps):
+        h.update(os.path.basename(d).encode())
+        with open(d, "rb") as f:
+            h.update(f.read())
+    h.update(" ".join(flags).encode())
+    try:
+        h.update(subprocess.run([nvcc(), "--version"], capture_output=True, text=True).stdout.encode())
+    except Exception:
+        pass
+    return h.hexdigest()
+
+
+def _up_to_date(lib: str, digest: str) -> bool:
+    try:
+        with open(lib + ".sha256") as f:
+            return os.path.exists(lib) and f.read().strip() == digest
+    except OSError:
         return False
-    t = os.path.getmtime(target)
-    return all(os.path.getmtime(d) <= t for d in deps)
 
 
 def check_no_stack(src: str, ptxas_log: str) -> None:
@@ -62,8 +84,10 @@ def check_no_stack(src: str, ptxas_log: str) -> None:
 def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB, build_dir: str = BUILD) -> str:
     """Builds the library. `defines` (debug experiments only, e.g. ("DS2CTC_EXP_NOOCC",))
     go to a separate `lib` / `build_dir`; the product library is built without any."""
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(INCLUDE, "ds2ctc.h"), __file__]
-    if not force and _newer(lib, deps):
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if os.path.isfile(os.path.join(CSRC, f))]
+    deps += [os.path.join(INCLUDE, f) for f in os.listdir(INCLUDE) if f.endswith((".h", ".hpp"))] + [__file__]
+    digest = _content_hash(deps, [*ARCH, *defines])
+    if not force and _up_to_date(lib, digest):
         return lib
     LIB_ = lib
     BUILD_ = build_dir
@@ -74,7 +98,8 @@ def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB
     objs = []
     for src in CU_SOURCES:
         obj = os.path.join(BUILD_, src + ".o")
-        cmd = [cc, *ARCH, "-lineinfo", "-Xptxas", "-v", *common, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [cc, *ARCH, "-lineinfo", "-Xptxas", "-v", *CU_FLAGS.get(src, []), *common, "-c", os.path.join(CSRC, src),
+               "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed:\n{' '.join(cmd)}\n{res.stderr}")
@@ -95,6 +120,8 @@ def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB
     subprocess.run([cc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-lpthread", "-ldl", "-lrt"],
                    check=True)
     os.replace(tmp, LIB_)
+    with open(LIB_ + ".sha256", "w") as f:
+        f.write(digest + "\n")
     return LIB_
 
 

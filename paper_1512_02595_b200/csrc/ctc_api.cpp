@@ -50,7 +50,10 @@ class Staging {
   }
 
  private:
-  static constexpr int kSlots = 8;
+  // Four calls' worth of blobs: a length-split call takes one slot per
+  // sub-batch (kDevSplitMax), so the host can still run several calls ahead
+  // of the GPU before acquire() waits on a slot's previous copy.
+  static constexpr int kSlots = 32;
   struct Slot {
     void* ptr = nullptr;
     size_t cap = 0;
@@ -597,8 +600,19 @@ ds2ctc_status run_split(const float* acts, float* grads, const int* flat_labels,
   } suspend{prof};
   prof.suspended = true;
   if (cudaEventRecord(ss.fork, s0) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
-  for (int c = 1; c < p.n; ++c)
-    if (cudaStreamWaitEvent(ss.s[c - 1], ss.fork, 0) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  int forked = 1;  // streams ordered after the fork (s0 itself is #0)
+  for (; forked < p.n; ++forked)
+    if (cudaStreamWaitEvent(ss.s[forked - 1], ss.fork, 0) != cudaSuccess) break;
+  // Every forked stream joins back into s0, on the error path as well, so the
+  // caller's stream stays ordered after whatever the sub-batches enqueued.
+  auto join = [&](ds2ctc_status result) {
+    for (int c = 1; c < forked; ++c)
+      if (cudaEventRecord(ss.join[c - 1], ss.s[c - 1]) != cudaSuccess ||
+          cudaStreamWaitEvent(s0, ss.join[c - 1], 0) != cudaSuccess)
+        result = DS2CTC_STATUS_EXECUTION_FAILED;
+    return result;
+  };
+  if (forked < p.n) return join(DS2CTC_STATUS_EXECUTION_FAILED);
   int t_max = 0;
   for (int b = 0; b < B; ++b) t_max = std::max(t_max, input_lengths[b]);
   for (int c = 0; c < p.n; ++c) {
@@ -612,17 +626,15 @@ ds2ctc_status run_split(const float* acts, float* grads, const int* flat_labels,
         cudaMemset2DAsync(grads + static_cast<size_t>(t_c) * B * A + col, pitch, 0,
                           static_cast<size_t>(p.b0[c + 1] - p.b0[c]) * A * sizeof(float), t_max - t_c,
                           c == 0 ? s0 : ss.s[c - 1]) != cudaSuccess)
-      return DS2CTC_STATUS_EXECUTION_FAILED;
+      return join(DS2CTC_STATUS_EXECUTION_FAILED);
     st = run(acts + col, grads ? grads + col : nullptr, flat_labels + p.lab0[c], label_lengths + p.b0[c],
              input_lengths + p.b0[c], A, p.b0[c + 1] - p.b0[c], blank, costs + p.b0[c],
              static_cast<unsigned char*>(workspace) + p.ws_off[c], p.ws_off[c + 1] - p.ws_off[c], true,
              c == 0 ? stream : ss.s[c - 1], B);
-    if (st != DS2CTC_STATUS_SUCCESS) return st;
+    if (st != DS2CTC_STATUS_SUCCESS) return join(st);
   }
-  for (int c = 1; c < p.n; ++c)
-    if (cudaEventRecord(ss.join[c - 1], ss.s[c - 1]) != cudaSuccess ||
-        cudaStreamWaitEvent(s0, ss.join[c - 1], 0) != cudaSuccess)
-      return DS2CTC_STATUS_EXECUTION_FAILED;
+  st = join(DS2CTC_STATUS_SUCCESS);
+  if (st != DS2CTC_STATUS_SUCCESS) return st;
   if (timed) {
     prof.mark(1, s0);
     prof.mark(2, s0);
@@ -747,6 +759,12 @@ ds2ctc_status ds2ctc_loss_sum_allreduce(const float* costs, int minibatch, doubl
   return DS2CTC_STATUS_SUCCESS;
 }
 
+ds2ctc_status ds2ctc_reduce_fault(unsigned long long* seq) {
+  if (seq == nullptr) return DS2CTC_STATUS_INVALID_VALUE;
+  if (read_reduce_fault(seq) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  return DS2CTC_STATUS_SUCCESS;
+}
+
 ds2ctc_status ds2ctc_loss_sum(const float* costs, int minibatch, double* out2, void* stream) {
   if (minibatch < 0 || out2 == nullptr || (minibatch > 0 && costs == nullptr)) return DS2CTC_STATUS_INVALID_VALUE;
   if (launch_loss_sum(costs, minibatch, out2, stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
@@ -854,6 +872,15 @@ ds2ctc_status ds2ctc_compute_loss_host(const float* activations, float* gradient
       return DS2CTC_STATUS_EXECUTION_FAILED;
 
   const size_t row = static_cast<size_t>(B) * A * sizeof(float);
+  // The contract is synchronous: on an error after some chunk was enqueued,
+  // drain every chunk stream before returning, so no queued copy touches the
+  // caller's host buffers after the call.
+  auto drain = [&](ds2ctc_status result) {
+    for (int c = 0; c < nc; ++c)
+      if (cudaStreamSynchronize(c == 0 ? ctx.stream : ctx.chunk_streams[c - 1]) != cudaSuccess)
+        result = result == DS2CTC_STATUS_SUCCESS ? DS2CTC_STATUS_EXECUTION_FAILED : result;
+    return result;
+  };
   for (int c = 0; c < nc; ++c) {
     cudaStream_t sc = c == 0 ? ctx.stream : ctx.chunk_streams[c - 1];
     const int bc = b0[c + 1] - b0[c];
@@ -866,26 +893,23 @@ ds2ctc_status ds2ctc_compute_loss_host(const float* activations, float* gradient
     const auto* xh = reinterpret_cast<const unsigned char*>(activations) + static_cast<size_t>(b0[c]) * A * sizeof(float);
     if (t_c[c] > 0 && w > 0 &&
         cudaMemcpy2DAsync(xd, xpitch, xh, row, w, t_c[c], cudaMemcpyHostToDevice, sc) != cudaSuccess)
-      return DS2CTC_STATUS_MEMOPS_FAILED;
+      return drain(DS2CTC_STATUS_MEMOPS_FAILED);
     float* cd = static_cast<float*>(ctx.costs) + b0[c];
     st = run(reinterpret_cast<const float*>(xd), reinterpret_cast<float*>(gd), flat_labels + lab0[c],
              label_lengths + b0[c], input_lengths + b0[c], A, bc, blank_label, cd,
              static_cast<unsigned char*>(ctx.ws) + ws_off[c], ws_off[c + 1] - ws_off[c], true, sc, direct ? B : 0);
-    if (st != DS2CTC_STATUS_SUCCESS) return st;
+    if (st != DS2CTC_STATUS_SUCCESS) return drain(st);
     if (gradients && t_c[c] > 0 && w > 0) {
       auto* gh = reinterpret_cast<unsigned char*>(gradients) + static_cast<size_t>(b0[c]) * A * sizeof(float);
       if (!direct && cudaMemcpy2DAsync(gh, row, gd, w, w, t_c[c], cudaMemcpyDeviceToHost, sc) != cudaSuccess)
-        return DS2CTC_STATUS_MEMOPS_FAILED;
+        return drain(DS2CTC_STATUS_MEMOPS_FAILED);
       // frames past this chunk's longest utterance: zero rows (the contract), on the host
       for (int t = t_c[c]; t < lay.t_max; ++t) std::memset(gh + static_cast<size_t>(t) * row, 0, w);
     }
     if (bc > 0 && cudaMemcpyAsync(costs + b0[c], cd, bc * sizeof(float), cudaMemcpyDeviceToHost, sc) != cudaSuccess)
-      return DS2CTC_STATUS_MEMOPS_FAILED;
+      return drain(DS2CTC_STATUS_MEMOPS_FAILED);
   }
-  for (int c = 0; c < nc; ++c)
-    if (cudaStreamSynchronize(c == 0 ? ctx.stream : ctx.chunk_streams[c - 1]) != cudaSuccess)
-      return DS2CTC_STATUS_EXECUTION_FAILED;
-  return DS2CTC_STATUS_SUCCESS;
+  return drain(DS2CTC_STATUS_SUCCESS);
 }
 
 // Host-buffer forms of the alignment and lattice export (the C++ shim's

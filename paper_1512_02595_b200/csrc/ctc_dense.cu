@@ -169,17 +169,30 @@ __global__ void k_finalize(PairArgs a) {
     a.costs[b] = lz == -__builtin_huge_val()
                      ? __builtin_huge_valf()
                      : static_cast<float>((acc + (a.part[2 * b] + a.part[2 * b + 1])) - lz * kLn2);
+  // A poisoned row (NaN / +inf logit, or all -inf: its lse is NaN, k_dense
+  // already wrote the row itself as NaN) makes log p NaN in the reference, so
+  // grad_column (ctc.cpp:69-79) writes NaN into every key column of every
+  // row: patch those <= L+1 columns per row (rare path; runs after k_dense).
+  if (a.grad != nullptr && acc != acc && lz != -__builtin_huge_val()) {
+    const float qnan = __int_as_float(0x7fc00000);
+    const int* keys = a.key_char + u.key_off;
+    for (int t = lane; t < u.T; t += 32) {
+      float* gr = a.grad + (static_cast<size_t>(t) * a.B + b) * a.A;
+      for (int j = 0; j < u.nkey; ++j) gr[keys[j]] = qnan;
+    }
+  }
 }
 
-// Trainer scalars (trainer.cpp:160-168): sum of finite costs, count of
-// infeasible ones; one warp, lane-strided then a fixed xor tree.
+// Trainer scalars (trainer.cpp:160-168): sum of feasible costs (NaN
+// included, as the reference adds res.loss), count of infeasible (+inf)
+// ones; one warp, lane-strided then a fixed xor tree.
 __global__ void k_loss_sum(const float* __restrict__ costs, int B, double* __restrict__ out2) {
   const int lane = threadIdx.x;
   double loss = 0.0, skipped = 0.0;
   for (int b = lane; b < B; b += 32) {
     const float c = costs[b];
-    if (isfinite(c)) loss += static_cast<double>(c);
-    else skipped += 1.0;
+    if (isinf(c) && c > 0.f) skipped += 1.0;  // infeasible is +inf only; NaN flows into the sum
+    else loss += static_cast<double>(c);
   }
   loss = warp_sum_d(loss);
   skipped = warp_sum_d(skipped);

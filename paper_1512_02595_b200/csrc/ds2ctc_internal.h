@@ -66,9 +66,10 @@ struct Geometry {
   int ring_depth; // halo refresh ring entries per chain warp
   int off_cb;     // column buffer [2][P][cw_max] floats (TMA bulk stores / loads of lattice columns)
   int off_mbar;   // two mbarriers (one per column-buffer half)
-  int off_dummy;  // write sink for chain threads without cells
+  int off_flag;   // poisoned-frame flags: [0] this CTA's phase-1 frames, [1] written by the partner at the meet
+  int off_nrm;    // [2][column_pitch(max_L)] per-thread frame mass of each phase-2 epoch's sampled column
   int xstride;    // floats per xraw row (odd)
-  int estride;    // floats per eb/el row (odd)
+  int estride;    // floats per occupancy (el) row (odd)
   int cw_max;     // floats per stored column (max over batch)
   int ostride;    // floats per occ scratch row (odd)
   int smem;       // total bytes
@@ -81,7 +82,7 @@ constexpr int kOwnedLanes = 32 - kHaloLanes;
 // The halo absorbs the wrong outer neighbour for 2*kHaloLanes*K rows, i.e.
 // kHaloLanes*K steps (the recursion moves 2 rows per step).
 DS2CTC_HD inline int halo_steps(int K) { return kHaloLanes * K < 16 ? kHaloLanes * K : 16; }
-DS2CTC_HD inline int column_threads(int L, int K);
+DS2CTC_HD inline int column_threads(int L, int K) { return (L + 1 + K - 1) / K; }
 DS2CTC_HD inline int chain_warps_for(int L, int K) { return (column_threads(L, K) + kOwnedLanes - 1) / kOwnedLanes; }
 
 // Label pairs per chain thread. At most three chain warps while K <= 8, so
@@ -95,12 +96,25 @@ inline int pick_K(int max_L) {
   return 8;
 }
 
-// Stored half-lattice column: chain thread j owns 2K consecutive slots
-// (forward: slot = cell s; backward: slot = s + 1, so each thread's cells are
-// 16-byte aligned), then one fp32 offset per chain thread.
-DS2CTC_HD inline int column_threads(int L, int K) { return (L + 1 + K - 1) / K; }
-DS2CTC_HD inline int column_offsets_base(int L, int K) { return round_up(2 * K * column_threads(L, K), 4); }
-DS2CTC_HD inline int column_width(int L, int K) { return column_offsets_base(L, K) + round_up(column_threads(L, K), 4); }
+// Stored half-lattice column, slot-major ("transposed"): chain thread j's
+// q-th slot (q < 2K) sits at q * W + j, then one fp32 offset per chain thread
+// at 2K * W + j (forward: slot = cell s; backward: slot = s + 1). Consecutive
+// lanes touch consecutive words on every access -- the per-step stores of
+// the owning warp and the partner's phase-2 reads -- so neither has shared-
+// memory bank conflicts (the thread-major layout of round 1 gave 2K-way
+// conflicts on the partner reads, profiles/r02_bank_conflicts.txt). W has
+// one spare column so the last thread's "next thread" reads stay in the row.
+DS2CTC_HD inline int column_pitch(int L, int K) { return round_up(column_threads(L, K) + 1, 4); }
+DS2CTC_HD inline int column_offsets_base(int L, int K) { return 2 * K * column_pitch(L, K); }
+DS2CTC_HD inline int column_width(int L, int K) { return (2 * K + 1) * column_pitch(L, K); }
+// Word index of stored slot `slot` in a column of pitch W.
+DS2CTC_HD inline int column_slot(int slot, int K, int W) { return (slot % (2 * K)) * W + slot / (2 * K); }
+// Occupancy rows (phase 2): label position li of a chain thread's K label
+// cells at (li % K) * WL + li / K with WL = ceil(L / K) -- again consecutive
+// across lanes; the spare slot K * WL takes the writes of cells without a label.
+DS2CTC_HD inline int occ_pitch(int L, int K) { return (L + K - 1) / K > 0 ? (L + K - 1) / K : 1; }
+DS2CTC_HD inline int occ_index(int li, int K, int WL) { return (li % K) * WL + li / K; }
+DS2CTC_HD inline int occ_row_words(int L, int K) { return K * occ_pitch(L, K) + 1; }
 
 // max_L_all: the longest label of the whole batch (it fixes K and hence the
 // stored column layout, see make_layout); max_L: the longest that runs.
@@ -115,7 +129,7 @@ inline Geometry make_geometry(int max_L_all, int max_L, int max_nkey, int A, boo
   for (int P = 32; P >= 2; P /= 2) {
     g.P = P;
     g.xstride = g.SW | 1;
-    g.estride = (max_L + 1) | 1;
+    g.estride = occ_row_words(max_L, g.K) | 1;
     g.ostride = max_nkey | 1;
     int off = 0;
     auto take = [&](int bytes) {
@@ -134,11 +148,12 @@ inline Geometry make_geometry(int max_L_all, int max_L, int max_nkey, int A, boo
     g.off_ring = take(8 * g.nchain * g.ring_depth * kHaloLanes * (2 * g.K + 1));
     g.off_cb = take(4 * 2 * P * g.cw_max);
     g.off_mbar = take(16);
+    g.off_nrm = take(4 * 2 * column_pitch(max_L, g.K));
     // meta: labels (L+1), key_char (nkey), key_start (nkey+1), key_pos (L), slot of each label
     // position (L+1), symbol -> slot (A shorts, fused)
     g.off_meta = take(4 * (4 * max_L + 2 * max_nkey + 8) + (fused ? 2 * A : 0));
     g.off_red = take(8 * 72);
-    g.off_dummy = take(4 * 8 * (2 * g.K + 4));
+    g.off_flag = take(16);
     g.smem = off;
     if (static_cast<size_t>(off) <= kSmemBudget) break;
   }
@@ -274,6 +289,8 @@ inline ViterbiLayout make_viterbi_layout(const int* label_lengths, const int* in
 
 // Launchers (ctc_pair.cu / ctc_dense.cu / ctc_viterbi.cu). Return cudaError_t as int.
 int launch_pair(const PairArgs& a, void* stream);
+int launch_pair_k8(const PairArgs& a, void* stream);  // ctc_pair_k8.cu
+int read_watchdog_k8(unsigned long long* out4);
 int launch_dense(const PairArgs& a, bool write_grad, void* stream);
 int launch_finalize(const PairArgs& a, void* stream);
 int launch_loss_sum(const float* costs, int B, double* out2, void* stream);
@@ -288,6 +305,7 @@ struct PeerMailboxes {
 int launch_loss_allreduce(const float* costs, int B, double* out2, const PeerMailboxes& mb, unsigned long long seq,
                           void* stream);
 size_t mailbox_bytes(int world);
+int read_reduce_fault(unsigned long long* seq);
 int read_watchdog(unsigned long long* out4);
 size_t viterbi_smem_bytes(int T, int L);
 int launch_viterbi(const ViterbiArgs& a, size_t smem, void* stream);

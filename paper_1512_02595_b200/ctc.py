@@ -147,7 +147,7 @@ def ctc_loss(frame_logits, label: Sequence[int], blank: int, device: int = 0) ->
     lab = list(int(c) for c in label)
     costs, grads = compute_ctc_loss_host(x.reshape(T, 1, A), lab, [len(lab)], [T], blank=blank, device=device)
     loss = float(costs[0])
-    if not np.isfinite(loss):
+    if np.isposinf(loss):  # infeasible (ctc.cpp:173,189-193); a NaN loss is feasible, as in the reference
         return CtcResult(False, float("inf"), np.zeros((0, 0), dtype=np.float32))
     return CtcResult(True, loss, grads.reshape(T, A))
 

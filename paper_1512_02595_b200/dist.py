@@ -40,14 +40,15 @@ def reduce_loss_skipped(local_loss: float, local_skipped: int, device=None) -> T
 
 
 def local_loss_skipped(costs: np.ndarray) -> Tuple[float, int]:
-    """trainer.cpp:160-168: infeasible utterances are skipped, the rest summed (in order)."""
+    """trainer.cpp:160-168: infeasible utterances (cost +inf) are skipped, the rest summed
+    in order -- a NaN cost (diverged logits) is feasible in the reference and makes the sum NaN."""
     loss = 0.0
     skipped = 0
     for c in np.asarray(costs, dtype=np.float64):
-        if np.isfinite(c):
-            loss += float(c)
-        else:
+        if np.isposinf(c):
             skipped += 1
+        else:
+            loss += float(c)
     return loss, skipped
 
 
@@ -123,12 +124,25 @@ class PeerLossReducer:
     def reduce(self, costs_ptr: int, B: int, out2_ptr: int, stream_ptr: int) -> None:
         from . import _lib
 
+        if self.own is None:
+            raise RuntimeError("PeerLossReducer is closed (a peer was lost); rebuild it on every rank")
         self.seq += 1
         _lib.check(self.lib.ds2ctc_loss_sum_allreduce(ctypes.c_void_p(costs_ptr), B, ctypes.c_void_p(out2_ptr),
                                                       ctypes.cast(self.ptrs, ctypes.POINTER(ctypes.c_void_p)),
                                                       self.rank, self.world, self.seq,
                                                       ctypes.c_void_p(stream_ptr)),
                    "ds2ctc_loss_sum_allreduce")
+
+    def check(self) -> None:
+        """Raises (and closes the mailboxes) if a step's peer wait timed out. The
+        kernel wrote NaN for that step instead of a stale fold; after a timeout
+        the one-step-ahead invariant is gone, so the reducer must be rebuilt."""
+        from . import _lib
+
+        seq = _lib.reduce_fault()
+        if seq is not None:
+            self.close()
+            raise RuntimeError(f"fused loss all-reduce: peer wait timed out at step {seq}")
 
     def close(self) -> None:
         for p in self.opened:

@@ -1,5 +1,10 @@
-"""The header-only C++ drop-in shim (include/ds2ctc.hpp) driven from C++,
-checked against the oracle (tests/cpp/shim_test.cpp)."""
+"""The header-only C++ drop-in shim (include/ds2ctc.hpp) driven from C++:
+checked against the oracle (tests/cpp/shim_test.cpp), and with the
+reference's OWN types and test cases (tests/cpp/ref_dropin_test.cpp:
+asr::Matrix / asr::ctc::CtcResult / asr::ctc::CtcLattice, the cases of
+proj/tests/test_ctc.cpp, checked against ctc_loss_reference and the
+reference's test oracles). The latter is built where /root/reference exists
+(this container: build() / tests/cpp/Makefile) and shipped prebuilt."""
 import os
 import subprocess
 
@@ -7,6 +12,7 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 EXE = os.path.join(ROOT, "build", "tests", "shim_test")
+REF_EXE = os.path.join(ROOT, "build", "tests", "ref_dropin_test")
 
 
 def test_cpp_shim_builds():
@@ -21,4 +27,20 @@ def test_cpp_shim_parity():
     res = subprocess.run([EXE], capture_output=True, text=True, timeout=300)
     print(res.stdout)
     assert res.returncode == 0, res.stdout + res.stderr
+    assert "PASS" in res.stdout
+
+
+def test_ref_dropin_builds_where_reference_exists():
+    if not os.path.isdir("/root/reference/proj"):
+        pytest.skip("reference sources absent (GPU box): the binary ships prebuilt")
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], check=True)
+    assert os.path.exists(REF_EXE)
+
+
+@pytest.mark.gpu
+def test_ref_dropin_with_reference_types():
+    assert os.path.exists(REF_EXE), "build/tests/ref_dropin_test missing: run build() where /root/reference exists"
+    res = subprocess.run([REF_EXE], capture_output=True, text=True, timeout=600)
+    print(res.stdout[-4000:])
+    assert res.returncode == 0, res.stdout[-4000:] + res.stderr[-2000:]
     assert "PASS" in res.stdout

@@ -1,0 +1,10 @@
+set -u
+O=gpurun_out/r02f; mkdir -p $O
+for v in head base noframemass nopoison noframemass_nonorm_nopoison; do
+  echo "== $v" >> $O/epoch.txt
+  timeout 300 python -c "
+import sys; sys.argv=['x']; sys.path.insert(0,'tools/epoch_timing')
+import build_and_run as b
+b.run('build/epoch_timing/libds2ctc_timing_$v.so', brief=True)" 2>&1 | grep -E "cta0|TIGHT" >> $O/epoch.txt
+done
+TAG=r02f VARIANTS="head noall nopoison nofm cur" ROUNDS=2 bash tools/ab_bench.sh > /dev/null 2>&1
