@@ -243,6 +243,27 @@ std::pair<int, int> build_metadata(const Layout& lay, const int* flat_labels, co
   return {max_L, max_nkey};
 }
 
+int sm_count() {
+  static int n[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (n[dev] == 0 && cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n[dev] = 148;
+  return n[dev];
+}
+
+// DS2CTC_DUAL: 0 = never two clusters per SM pair, 1 = whenever it fits,
+// default: when the batch needs more than one wave (2B > SMs).
+bool dual_mode(int B) {
+  static const int env = [] {
+    const char* v = std::getenv("DS2CTC_DUAL");
+    return v ? std::atoi(v) : -1;
+  }();
+  if (env == 0) return false;
+  if (env > 0) return true;
+  return 2 * B > sm_count();
+}
+
 ds2ctc_status run(const float* acts, float* grads, const int* flat_labels, const int* label_lengths,
                   const int* input_lengths, int A, int B, int blank, float* costs, void* workspace,
                   size_t workspace_bytes, bool check_ws, void* stream, int ld = 0) {
@@ -296,6 +317,17 @@ ds2ctc_status run(const float* acts, float* grads, const int* flat_labels, const
   for (int b = 0; b < B; ++b) max_L_all = std::max(max_L_all, label_lengths[b]);
   a.g = make_geometry(max_L_all, mx.first, mx.second, A, fused);
   if (static_cast<size_t>(a.g.smem) > kSmemBudget) return DS2CTC_STATUS_UNSUPPORTED;
+  // Multi-wave batches (more clusters than SM pairs): two clusters per SM
+  // pair when the geometry fits half the shared memory with epochs of >= 8
+  // steps and <= 3 chain warps (K <= 4) -- the chains are latency-bound, so a
+  // second resident utterance uses issue slots the first leaves idle.
+  if (dual_mode(B) && a.g.K <= 4 && a.g.nchain <= 3) {
+    const Geometry g2 = make_geometry(max_L_all, mx.first, mx.second, A, fused, kSmemBudgetDual);
+    if (static_cast<size_t>(g2.smem) <= kSmemBudgetDual && g2.P >= 8) {
+      a.g = g2;
+      a.g.dual = 1;
+    }
+  }
 
   int dev = 0;
   cudaGetDevice(&dev);

@@ -13,6 +13,9 @@ extern "C" int ds2ctc_debug_meet_clocks(long long* host) {
   if (e) return e;
   return cudaMemcpyFromSymbol(host + 16, g_kernel_end, sizeof(g_kernel_end));
 }
+extern "C" int ds2ctc_debug_prologue_clocks(long long* host) {
+  return cudaMemcpyFromSymbol(host, g_pro_clock, sizeof(g_pro_clock));
+}
 extern "C" int ds2ctc_debug_step_clocks(long long* host) {
   return cudaMemcpyFromSymbol(host, g_step_clock, sizeof(g_step_clock));
 }
@@ -32,6 +35,15 @@ int read_watchdog(unsigned long long* out4) {
 
 int launch_pair(const PairArgs& a, void* stream) {
   if (a.B == 0) return cudaSuccess;
+  if (a.g.dual) {
+    switch (a.g.K) {
+      case 1: return launch_k<1, 2>(a, stream);
+      case 2: return launch_k<2, 2>(a, stream);
+      case 3: return launch_k<3, 2>(a, stream);
+      case 4: return launch_k<4, 2>(a, stream);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (a.g.K) {
     case 1: return launch_k<1>(a, stream);
     case 2: return launch_k<2>(a, stream);

@@ -242,6 +242,13 @@ __device__ long long g_epoch_clock[2][128][33][2];
 __device__ long long g_step_clock[2][8][32][4];
 __device__ long long g_meet_clock[2][8];
 __device__ long long g_kernel_end[2];
+// prologue stamps [cta][point][warp 0..7]
+__device__ long long g_pro_clock[2][8][8];
+#define PRO_STAMP(i)                                                                          \
+  do {                                                                                        \
+    if (blockIdx.x < 2 && (threadIdx.x & 31) == 0 && (threadIdx.x >> 5) < 8)                  \
+      g_pro_clock[dir][i][threadIdx.x >> 5] = clock64();                                      \
+  } while (0)
 #define MEET_STAMP(i) \
   do {                \
     if (blockIdx.x < 2 && tid == 0) g_meet_clock[dir][i] = clock64(); \
@@ -266,6 +273,9 @@ __device__ long long g_kernel_end[2];
   } while (0)
 #define MEET_STAMP(i) \
   do {                \
+  } while (0)
+#define PRO_STAMP(i) \
+  do {               \
   } while (0)
 #endif
 
@@ -319,9 +329,6 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   const int T = u.T, L = u.L, S = u.S, tm = u.tm;
   const int P = g.P, RX = 4 * P, P2 = 2 * P;  // powers of two
   const int MX = RX - 1, M2 = P2 - 1;
-  const int OB = column_offsets_base(L, K);  // per-thread offsets of a stored column start here
-  const int CW = column_pitch(L, K);          // slot-major column: slot q of thread j at q * CW + j
-  const int WL = occ_pitch(L, K);             // occupancy rows: label li at (li % K) * WL + li / K
   const int cw = u.col_w;
   const int nw_u = chain_warps_for(L, K);  // chain warps this utterance uses
   const int SW = emis_stride(g.SW);  // emission row: staged symbols + the sentinel column g.SW (odd stride)
@@ -336,7 +343,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   float* el = reinterpret_cast<float*>(smem + g.off_el);
   float* occs = reinterpret_cast<float*>(smem + g.off_occ);
   float* nrm = reinterpret_cast<float*>(smem + g.off_nrm);  // [2][NPW] frame mass per chain thread
-  const int NPW = column_pitch(g.max_L, K);
+  const int NPW = column_threads(g.max_L, K);
   const int CT = column_threads(L, K);
   unsigned long long* ring = reinterpret_cast<unsigned long long*>(smem + g.off_ring);
   int* s_lab = reinterpret_cast<int*>(smem + g.off_meta);
@@ -370,12 +377,13 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
 
   // ---- prologue: per-utterance metadata into shared memory ----
   MEET_STAMP(6);
-  if (fused && warp == 0) {  // epoch 0's logit rows (no metadata needed): in flight during the prologue
+  if (fused) {  // epoch 0's logit rows (no metadata needed), issued by every thread: in flight during the prologue
     const int n0 = min(P, kmid + 1);
     const float* xu = a.x + static_cast<size_t>(b) * a.A;
-    for (int c = lane; c < a.A; c += 32)
-      for (int r = 0; r < n0; ++r)
-        cp_async4(xraw + (r & MX) * g.xstride + c, xu + static_cast<size_t>(dir == 0 ? r : T - 1 - r) * rs + c);
+    for (int q = tid; q < n0 * a.A; q += NT) {
+      const int r = q / a.A, c = q - r * a.A;
+      cp_async4(xraw + (r & MX) * g.xstride + c, xu + static_cast<size_t>(dir == 0 ? r : T - 1 - r) * rs + c);
+    }
     cp_async_commit();
   }
   for (int i = tid; i < L; i += NT) s_lab[i] = a.labels[u.lab_off + i];
@@ -384,6 +392,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   for (int q = tid; q < L; q += NT) s_kpos[q] = a.key_pos[u.lab_off + q];
   if (fused)
     for (int c = tid; c < a.A; c += NT) s_slot[c] = -1;
+  PRO_STAMP(0);
   for (int q = tid; q < NCW * g.ring_depth * kHaloLanes * (2 * K + 1); q += NT) ring[q] = ~0ull;
   if (tid == 0) {
     s_pflag[0] = 0u;
@@ -391,24 +400,27 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     mbar_init(cb_mbar + 1, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  cp_async_wait_all();  // this thread's share of epoch 0's rows
   __syncthreads();
-  if (fused)
-    for (int j = tid; j < u.nkey; j += NT) s_slot[s_kchar[j]] = static_cast<short>(j);
-  for (int j = tid; j < u.nkey; j += NT)
-    for (int q = s_kstart[j]; q < s_kstart[j + 1]; ++q) {
-      s_slotpos[s_kpos[q]] = j;
-      s_kq[q] = occ_index(s_kpos[q], K, WL) | (j << 16);  // the position's occupancy-row word
-    }
-  __syncthreads();
-
+  PRO_STAMP(1);
   auto frame = [&](int k) { return dir == 0 ? k : T - 1 - k; };
+  // Phase-2 epoch lengths: P, except that the last two epochs are Q = P / 4
+  // frames each -- after the loop the gradient warp still has to sum and write
+  // the last epoch's rows and the service warp the one before (the drain),
+  // which costs ~Q / P of a full epoch's helper work instead of all of it.
+  auto phase2_len = [&](int rem) {
+    const int Q = P >= 8 ? P / 4 : P;
+    if (rem <= Q) return rem;
+    if (rem <= 2 * Q) return rem - Q;
+    return min(P, rem - 2 * Q);
+  };
   auto next_epoch = [&](const Epoch& e) -> Epoch {
     if (e.phase == 1) {
       if (e.k1 <= kmid) return {e.k1, min(e.k1 + P, kmid + 1), 1};
-      if (want_grad && k2s < T) return {k2s, min(k2s + P, T), 2};
+      if (want_grad && k2s < T) return {k2s, k2s + phase2_len(T - k2s), 2};
       return {0, 0, 0};
     }
-    if (e.phase == 2 && e.k1 < T) return {e.k1, min(e.k1 + P, T), 2};
+    if (e.phase == 2 && e.k1 < T) return {e.k1, e.k1 + phase2_len(T - e.k1), 2};
     return {0, 0, 0};
   };
 
@@ -539,14 +551,43 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     }
     __syncwarp();
   };
+  // ---- prologue: epoch 0's rows -> emissions, on the service warp while the
+  // chain warps set up their lanes (below) ----
+  // ---- prologue, continued: the service warp turns epoch 0's rows into
+  // emissions while the other warps build the key maps ----
+  Epoch cur{0, min(P, kmid + 1), 1};
+  if (service) {
+    if (!fused) {  // split: the staged symbols are the key map's
+      stage(cur);
+      cp_async_wait_all();
+      __syncwarp();
+    }
+    PRO_STAMP(3);
+    convert(cur);
+  } else {
+    const int t2 = tid - 32, n2 = NT - 32;
+    if (fused)
+      for (int j = t2; j < u.nkey; j += n2) s_slot[s_kchar[j]] = static_cast<short>(j);
+    for (int j = t2; j < u.nkey; j += n2)
+      for (int q = s_kstart[j]; q < s_kstart[j + 1]; ++q) {
+        s_slotpos[s_kpos[q]] = j;
+        s_kq[q] = occ_word(s_kpos[q], K, dir) | (j << 16);  // the position's occupancy-row word
+      }
+  }
+  __syncthreads();
+  PRO_STAMP(2);
+
   // Gradient rows of a finished phase-2 epoch (ctc.cpp:196-203, 69-79) in two
   // stages on two warps: grad_occ (gradient warp, one epoch behind the
   // chain) sums the label occupancies per key slot into occs[half];
   // grad_write (service warp, one epoch later) forms softmax - occupancy and
   // stores the rows. Lane = row; all lanes walk the same (uniform) index
   // sequences, so every loop is divergence-free.
-  auto grad_occ = [&](const Epoch& e, int half) {
-    if (e.phase != 2) return;
+  // Label sums of slots [jlo, jhi) of the epoch's frames; returns this lane's
+  // (frame's) unnormalised total over them. The full call (all slots) also
+  // writes the blank slot; the drain splits the slots over several warps.
+  auto grad_occ_part = [&](const Epoch& e, int half, int jlo, int jhi, float& inv_out) -> float {
+    if (e.phase != 2) return 0.f;
     const int n = e.k1 - e.k0;
     const int k = e.k0 + (lane < n ? lane : 0);
     const float* elr = el + (k & M2) * g.estride;
@@ -573,10 +614,12 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
     const float inv = z > 0.5f && z < 2.f ? __frcp_rn(z) : 1.f;  // a sane mass, else leave as is
 #endif
+    inv_out = inv;
     float acc = 0.f, tot = 0.f;
-    int cur = 1;
-    int q = s_kstart[1];
-    for (; q + 3 < L; q += 4) {
+    int cur = jlo;
+    int q = s_kstart[jlo];
+    const int qend = s_kstart[jhi];
+    for (; q + 3 < qend; q += 4) {
       const int w0 = s_kq[q], w1 = s_kq[q + 1], w2 = s_kq[q + 2], w3 = s_kq[q + 3];
       const float v0 = elr[w0 & 0xFFFF], v1 = elr[w1 & 0xFFFF], v2 = elr[w2 & 0xFFFF], v3 = elr[w3 & 0xFFFF];
       const int j0 = w0 >> 16, j1 = w1 >> 16, j2 = w2 >> 16, j3 = w3 >> 16;
@@ -589,17 +632,23 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
       if (j3 != cur) { oc[cur] = acc * inv; tot += acc; acc = 0.f; cur = j3; }
       acc += v3;
     }
-    for (; q < L; ++q) {
+    for (; q < qend; ++q) {
       const int w0 = s_kq[q];
       const int j0 = w0 >> 16;
       if (j0 != cur) { oc[cur] = acc * inv; tot += acc; acc = 0.f; cur = j0; }
       acc += elr[w0 & 0xFFFF];
     }
-    if (u.nkey > 1) {
+    if (jhi > jlo) {
       oc[cur] = acc * inv;
       tot += acc;
     }
-    oc[0] = 1.f - tot * inv;
+    return tot;
+  };
+  auto grad_occ = [&](const Epoch& e, int half) {
+    if (e.phase != 2) return;
+    float inv = 1.f;
+    const float tot = grad_occ_part(e, half, 1, u.nkey, inv);
+    occs[(half * 32 + lane) * g.ostride] = 1.f - tot * inv;  // the blank slot
   };
   auto grad_write = [&](const Epoch& e, int half) {
     if (e.phase != 2) return;
@@ -607,16 +656,28 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     // one row per iteration, lane = symbol: reads conflict-free, stores coalesced
     if (fused) {
       float* gb = a.grad + static_cast<size_t>(b) * a.A;
-      for (int c = lane; c < a.A; c += 32) {
-        const int slot = s_slot[c];
+      // a poisoned utterance (rare) takes its own loop: no per-element select here
+      if (!upoison) {
+        for (int c = lane; c < a.A; c += 32) {
+          const int slot = s_slot[c];
 #pragma unroll 2
-        for (int r = 0; r < n; ++r) {
-          const int k = e.k0 + r;
-          const float2 st = lser[k & MX];
-          const float* oc = occs + (half * 32 + r) * g.ostride;
-          const float soft = ex2(((xraw[(k & MX) * g.xstride + c] - st.x) - st.y) * kL2eH);
-          const float oc_c = upoison ? __int_as_float(0x7fc00000) : oc[slot];
-          gb[static_cast<size_t>(frame(k)) * rs + c] = soft - (slot >= 0 ? oc_c : 0.f);
+          for (int r = 0; r < n; ++r) {
+            const int k = e.k0 + r;
+            const float2 st = lser[k & MX];
+            const float* oc = occs + (half * 32 + r) * g.ostride;
+            const float soft = ex2(((xraw[(k & MX) * g.xstride + c] - st.x) - st.y) * kL2eH);
+            gb[static_cast<size_t>(frame(k)) * rs + c] = soft - (slot >= 0 ? oc[slot] : 0.f);
+          }
+        }
+      } else {
+        for (int c = lane; c < a.A; c += 32) {
+          const bool key = s_slot[c] >= 0;
+          for (int r = 0; r < n; ++r) {
+            const int k = e.k0 + r;
+            const float2 st = lser[k & MX];
+            const float soft = ex2(((xraw[(k & MX) * g.xstride + c] - st.x) - st.y) * kL2eH);
+            gb[static_cast<size_t>(frame(k)) * rs + c] = key ? __int_as_float(0x7fc00000) : soft;
+          }
         }
       }
     } else {
@@ -822,19 +883,21 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
 #ifdef DS2CTC_EXP_NOSTORE
     return;
 #endif
-    // slot-major: slot q of this thread at q * CW + ctid -- each store of the
-    // warp covers consecutive words (conflict-free); threads without cells
-    // (halo lanes, lanes past the label) are predicated off
-    float* row = cb_row(k, e);
+    // warp-blocked: this lane's slots at one base + q * 32 (immediates), each
+    // store of the warp on consecutive words (conflict-free). Unconditional
+    // (no branch or predicate in the step's basic block): the words of halo
+    // lanes and of lanes past the label are never read (partner reads and the
+    // meet only touch threads that own cells).
+    float* dst = cb_row(k, e) + cwarp * column_block(K) + lane;
 #pragma unroll
     for (int p = 0; p < K; ++p) {
       const float cbv = dir == 0 ? vb[p] : xb[p];
       const float clv = dir == 0 ? vl[p] : xl[p];
       // forward pair = slots (blank 2i, label 2i+1); backward = (label 2i-1, blank 2i) at +1
-      sts1_if(stores, row + (2 * p) * CW + ctid, dir == 0 ? cbv : clv);
-      sts1_if(stores, row + (2 * p + 1) * CW + ctid, dir == 0 ? clv : cbv);
+      dst[(2 * p) * 32] = dir == 0 ? cbv : clv;
+      dst[(2 * p + 1) * 32] = dir == 0 ? clv : cbv;
     }
-    sts1_if(stores, row + OB + ctid, O);
+    dst[2 * K * 32] = O;
   };
 
   // Phase 2: label-cell occupancies from the partner's stored columns,
@@ -844,16 +907,24 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   // slot s + 1 (backward partner) or s (forward partner): this lane's label
   // cells 2i+1 (forward) sit at partner slots 2i+2, label cells 2i-1
   // (backward) at 2i-1; the last forward label belongs to the next thread.
-  int pslot[K];  // word of the partner slot in the slot-major column (consecutive across lanes)
+  // Partner words (the other direction's warp-blocked layout): consecutive
+  // across the lanes that own cells; lanes without a cell read lane 0's word
+  // instead (a broadcast, never a bank conflict). The partner thread of
+  // pslot / poff is ctid or its neighbour, so these are loop invariants.
+  const int pdir = dir ^ 1;
+  const int ctid0 = cwarp * kOwnedLanes;  // the warp's first owned thread
+  int pslot[K];
 #pragma unroll
-  for (int p = 0; p < K; ++p)  // lanes without the cell read any in-row word (their occupancy goes to the spare slot)
-    pslot[p] = has_l[p] ? column_slot(2 * K * ctid + 2 * p + (dir == 0 ? 2 : -1), K, CW) : 0;
-  int el_idx[K];  // occupancy-row word of each label cell (K * WL = the spare slot, never read)
-#pragma unroll
-  for (int p = 0; p < K; ++p) el_idx[p] = has_l[p] ? occ_index(dir == 0 ? ctid * K + p : ctid * K + p - 1, K, WL) : K * WL;
-  // writer threads of the first / last slot (clamped into the row for lanes without cells)
-  const int poff_lo = OB + min(max(dir == 0 ? ctid : ctid - 1, 0), CW - 1);
-  const int poff_hi = OB + min(max(dir == 0 ? ctid + 1 : ctid, 0), CW - 1);
+  for (int p = 0; p < K; ++p) {
+    const int sl = 2 * K * (has_l[p] ? ctid : ctid0) + 2 * p + (dir == 0 ? 2 : -1);
+    pslot[p] = column_slot_word(max(sl, 0), K, pdir);
+  }
+  // occupancy-row word of each label cell: this lane's own block slot
+  const int el_base = cwarp * K * 32 + lane;
+  // writer threads of the first / last slot
+  const int oct = owner ? ctid : ctid0;
+  const int poff_lo = column_word(max(dir == 0 ? oct : oct - 1, 0), 2 * K, K, pdir);
+  const int poff_hi = column_word(dir == 0 ? oct + 1 : oct, 2 * K, K, pdir);
   // The partner cells of the next row are fetched one step ahead.
   float pd[K], po_lo = 0.f, po_hi = 0.f;
 #pragma unroll
@@ -868,7 +939,10 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   // gamma = alpha + beta - log Z (plain add, ctc.cpp:200), in log2 units; the
   // carried offset was shifted by -log Z at the meet, so the offsets add
   // exactly and only the residuals round; the occupancy row holds 2^gamma.
-  auto occupancy_column = [&](int k, const Epoch& e) {
+  // `full` (the epoch's last column only): the blank cells too, and this
+  // thread's share of sum_s 2^gamma(s, t) for the gradient warp's per-frame
+  // renormalisation (grad_occ).
+  auto occupancy_column = [&](int k, const Epoch& e, bool full) {
 #ifdef DS2CTC_EXP_NOOCC
     return;
 #endif
@@ -876,37 +950,29 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     float d[K];
 #pragma unroll
     for (int p = 0; p < K; ++p) d[p] = pd[p];
-    partner_fetch(min(k + 1, e.k1 - 1), e);
+    if (!full) partner_fetch(min(k + 1, e.k1 - 1), e);
     float* elr = el + (k & M2) * g.estride;
-#pragma unroll
-    for (int p = 0; p < K; ++p) {
-      const float rl = dir == 0 ? vl[p] : xl[p];
-      const float ol = (dir == 0 ? p == K - 1 : p != 0) ? o_hi : o_lo;
-      // linear occupancy 2^gamma; unconditional: cells without a label write the row's spare slot L
-      elr[el_idx[p]] = ex2(ol + (rl + d[p]));
-    }
-  };
-
-  // The epoch's last column once more, over ALL its cells (blank ones too):
-  // each chain thread's share of sum_s 2^gamma(s, t), for the gradient
-  // warp's per-frame renormalisation (grad_occ). Once per epoch, after the
-  // column's own occupancy pass; the carried values are that column's.
-  auto frame_mass = [&](int k, const Epoch& e) {
-    const float* row = cb_row(k, e);
-    const float o_lo = row[poff_lo] + O, o_hi = row[poff_hi] + O;
     float tot = 0.f;
 #pragma unroll
     for (int p = 0; p < K; ++p) {
       const float rl = dir == 0 ? vl[p] : xl[p];
       const float ol = (dir == 0 ? p == K - 1 : p != 0) ? o_hi : o_lo;
-      const float ml = ex2(ol + (rl + row[pslot[p]]));
-      // blank 2i: forward partner slot 2i + 1, backward partner slot 2i (both thread ctid)
-      const int bw = (dir == 0 ? 2 * p + 1 : 2 * p) * CW + max(ctid, 0);
-      const float rb = dir == 0 ? vb[p] : xb[p];
-      const float mb = ex2((dir == 0 ? o_lo : o_hi) + (rb + row[bw]));
-      tot += (has_l[p] ? ml : 0.f) + (has_b[p] ? mb : 0.f);
+      // linear occupancy 2^gamma; unconditional: cells without a label write their own unused word
+      const float ml = ex2(ol + (rl + d[p]));
+      elr[el_base + p * 32] = ml;
+#ifndef DS2CTC_EXP_NOFRAMEMASS
+      if (full) {
+        // blank 2i: forward partner slot 2i + 1, backward partner slot 2i (both thread ctid)
+        const float* row = cb_row(k, e);
+        const float rb = dir == 0 ? vb[p] : xb[p];
+        const float mb = ex2((dir == 0 ? o_lo : o_hi) + (rb + row[column_word(oct, dir == 0 ? 2 * p + 1 : 2 * p, K, pdir)]));
+        tot += (has_l[p] ? ml : 0.f) + (has_b[p] ? mb : 0.f);
+      }
+#endif
     }
-    if (stores) nrm[(ep & 1) * NPW + ctid] = tot;
+#ifndef DS2CTC_EXP_NOFRAMEMASS
+    if (full && stores) nrm[(ep & 1) * NPW + ctid] = tot;
+#endif
   };
 
   // Steps [k0, k1) of one epoch. Step k computes column k and finishes
@@ -942,7 +1008,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
         for (; k < kb; ++k) {
           STEP_STAMP(k, e, 0);
           const Nb nb = neighbour(k);
-          occupancy_column(k - 1, e);
+          occupancy_column(k - 1, e, false);
           step(k, nb);
           load_emis(k + 1);
           STEP_STAMP(k, e, 2);
@@ -963,25 +1029,15 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
       }
     }
     if (ph2) {
-      occupancy_column(e.k1 - 1, e);
-#ifndef DS2CTC_EXP_NOFRAMEMASS
-      frame_mass(e.k1 - 1, e);
-#endif
+      occupancy_column(e.k1 - 1, e, true);
     } else {
       store_column(e.k1 - 1, e);
       fence_async_shared();  // the service warp bulk-stores this epoch's columns
     }
   };
 
-  // ---- prologue staging of epoch 0 ----
-  Epoch cur{0, min(P, kmid + 1), 1};
-  if (service) {
-    if (!fused) stage(cur);  // fused: issued at the top of the prologue
-    cp_async_wait_all();
-    __syncwarp();
-    convert(cur);
-  }
-  __syncthreads();
+  PRO_STAMP(4);
+  __syncthreads();  // epoch 0's emissions (service warp, above) and every chain lane's setup
 
   Epoch prev{0, 0, 0}, prev2{0, 0, 0};
   bool dead = false;
@@ -1051,44 +1107,43 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
         bulk_wait0();  // every stored column is in global memory before the partner reads it
         // our phase-1 frames' poison flag into the partner's s_pflag[1] (the
         // cluster barrier below orders it before the partner's read)
+#ifndef DS2CTC_EXP_NOPOISON
         st_cluster_u32(const_cast<unsigned*>(s_pflag + 1), dir ^ 1u, s_pflag[0]);
+#endif
       }
       MEET_STAMP(1);
       cluster_barrier();
+#ifndef DS2CTC_EXP_NOPOISON
       upoison = (s_pflag[0] | s_pflag[1]) != 0u;
+#endif
       MEET_STAMP(2);
       // Both CTAs read the two STORED columns (alpha(tm) at column T, beta(tm)
       // at column tm) with the same cell->thread map and reduction order, so
       // they derive the bitwise-identical log Z.
       const float* ca = a.store + u.store_off + static_cast<size_t>(T) * cw;
       const float* cbp = a.store + u.store_off + static_cast<size_t>(tm) * cw;
-      // Cell s sits in slot s (forward column) and slot s + 1 (backward); the
-      // slot-major word of slot q*... is walked incrementally (thread j, slot
-      // q within the thread): ptxas 12.9 for sm_100a segfaults on the
-      // division form of this index inside these loops.
-      struct Walk {
-        int j, q;  // forward slot s = thread j, slot q; backward slot s + 1 follows
+      // Cell s sits in slot s of the forward column and slot s + 1 of the
+      // backward one. The cells are walked in forward-column word order (lane
+      // fastest), so each warp's loads of both columns are coalesced.
+      const int nwords = nw_u * 2 * K * 32;
+      auto cell_of = [&](int w) -> int {  // forward word -> cell (-1: not a cell)
+        const int bw = w / (2 * K * 32), q = (w / 32) % (2 * K), l = w % 32;
+        const int j = bw * kOwnedLanes + l - kHaloLanes;
+        const int sc = 2 * K * j + q;
+        return l >= kHaloLanes && sc < S ? sc : -1;
       };
-      auto walk0 = [&]() -> Walk { return {tid / (2 * K), tid % (2 * K)}; };
-      const int dj = NT / (2 * K), dq = NT % (2 * K);
-      auto advance = [&](Walk& w) {
-        w.j += dj;
-        w.q += dq;
-        if (w.q >= 2 * K) { w.q -= 2 * K; ++w.j; }
-      };
-      auto cell = [&](const Walk& w) -> double {
-        const int jb = w.q + 1 < 2 * K ? w.j : w.j + 1, qb = w.q + 1 < 2 * K ? w.q + 1 : 0;
-        const float wa = ca[OB + w.j], da = ca[w.q * CW + w.j];   // forward: slot s
-        const float wb = cbp[OB + jb], db = cbp[qb * CW + jb];      // backward: slot s + 1
+      auto cell = [&](int s) -> double {
+        const int ja = s / (2 * K), jb = (s + 1) / (2 * K);
+        const float wa = ca[column_word(ja, 2 * K, K, 0)], da = ca[column_slot_word(s, K, 0)];
+        const float wb = cbp[column_word(jb, 2 * K, K, 1)], db = cbp[column_slot_word(s + 1, K, 1)];
         return (static_cast<double>(wa) + static_cast<double>(da)) + (static_cast<double>(wb) + static_cast<double>(db));
       };
       double mloc = -__builtin_huge_val();
-      {
-        Walk w = walk0();
-        for (int s = tid; s < S; s += NT, advance(w)) {
-          const double v = cell(w);
-          if (v > kSentCutD) mloc = v > mloc ? v : mloc;  // sentinel cells are -inf
-        }
+      for (int w = tid; w < nwords; w += NT) {
+        const int sc = cell_of(w);
+        if (sc < 0) continue;
+        const double v = cell(sc);
+        if (v > kSentCutD) mloc = v > mloc ? v : mloc;  // sentinel cells are -inf
       }
       for (int o = 16; o > 0; o >>= 1) {
         const double w = __shfl_xor_sync(0xffffffffu, mloc, o);
@@ -1102,9 +1157,10 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
         logz2 = M;
       } else {
         float sl = 0.f;
-        Walk w = walk0();
-        for (int s = tid; s < S; s += NT, advance(w)) {
-          const double v = cell(w);
+        for (int w = tid; w < nwords; w += NT) {
+          const int sc = cell_of(w);
+          if (sc < 0) continue;
+          const double v = cell(sc);
           if (v > kSentCutD) sl += ex2(static_cast<float>(v - M));
         }
         for (int o = 16; o > 0; o >>= 1) sl += __shfl_xor_sync(0xffffffffu, sl, o);
@@ -1157,14 +1213,29 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   // drain: the last two epochs' gradient rows (grad_occ runs one epoch behind
   // the chain, grad_write two); CTA-uniform condition
   if (!dead && want_grad) {
-    // the gradient warp finishes the last epoch itself (its label sums are
-    // its own writes), the service warp the one before, concurrently
+    // The last epoch's label sums on the gradient warp AND the (idle) chain
+    // warps, each a contiguous range of key slots, while the service warp
+    // writes the rows of the epoch before; then the gradient warp forms the
+    // blank slot from the parts' totals and writes the last rows.
+    const int nparts = NCW + 1;
+    const int part = grad_warp ? 0 : warp;  // chain warps are 1..NCW
+    float* red_f = reinterpret_cast<float*>(red);
+    if (grad_warp || (warp >= 1 && warp <= NCW)) {
+      const int ns = u.nkey - 1;
+      float inv = 1.f;
+      const float t = grad_occ_part(prev, (ep - 1) & 1, 1 + ns * part / nparts, 1 + ns * (part + 1) / nparts, inv);
+      red_f[part * 32 + lane] = t;
+      if (grad_warp) red_f[nparts * 32 + lane] = inv;
+    }
+    if (service) grad_write(prev2, (ep - 2) & 1);
+    __syncthreads();
     if (grad_warp) {
-      grad_occ(prev, (ep - 1) & 1);
+      float tot = 0.f;
+      for (int pp = 0; pp < nparts; ++pp) tot += red_f[pp * 32 + lane];
+      occs[(((ep - 1) & 1) * 32 + lane) * g.ostride] = 1.f - tot * red_f[nparts * 32 + lane];
       __syncwarp();
       grad_write(prev, (ep - 1) & 1);
     }
-    if (service) grad_write(prev2, (ep - 2) & 1);
     __syncthreads();
   }
 
@@ -1190,28 +1261,32 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   }
 }
 
-template <int K>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(max_threads_for<K>(), 1) k_pair(PairArgs a) {
+// MINB = 2: the "dual" build for multi-wave batches -- two clusters per SM
+// pair (<= 200 registers, the geometry's shared memory <= kSmemBudgetDual),
+// so a second utterance's latency-bound chain fills the issue slots the
+// first leaves idle.
+template <int K, int MINB>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MINB == 2 ? 160 : max_threads_for<K>(), MINB)
+    k_pair(PairArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   if (cluster_rank() == 0) pair_body<K, 0>(a, smem);
   else pair_body<K, 1>(a, smem);
 }
-
-template <int K>
+template <int K, int MINB = 1>
 int launch_k(const PairArgs& a, void* stream) {
   const int threads = 32 * (a.g.nchain + 2);
-  if (threads > max_threads_for<K>()) return cudaErrorInvalidValue;
-  // The dynamic shared-memory opt-in is set once per (device, K) to the budget.
+  if (threads > (MINB == 2 ? 160 : max_threads_for<K>())) return cudaErrorInvalidValue;
+  // The dynamic shared-memory opt-in is set once per (device, K, MINB) to the budget.
   static int configured[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || !configured[dev]) {
-    cudaError_t err = cudaFuncSetAttribute(k_pair<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(kSmemBudget));
+    cudaError_t err = cudaFuncSetAttribute(k_pair<K, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(MINB == 2 ? kSmemBudgetDual : kSmemBudget));
     if (err != cudaSuccess) return err;
     if (dev >= 0 && dev < 64) configured[dev] = 1;
   }
-  k_pair<K><<<2 * a.B, threads, a.g.smem, static_cast<cudaStream_t>(stream)>>>(a);
+  k_pair<K, MINB><<<2 * a.B, threads, a.g.smem, static_cast<cudaStream_t>(stream)>>>(a);
   return cudaGetLastError();
 }
 

@@ -29,6 +29,9 @@ constexpr int kFusedMaxAlphabet = 128;
 constexpr int kMaxThreads = 384;  // <= 10 chain warps (K = 8, L <= 2047) + service + gradient warps
 constexpr size_t kAlign = 256;
 constexpr size_t kSmemBudget = 220 * 1024;
+// Two CTAs per SM (the dual build for multi-wave batches): 228 KB per SM,
+// 1 KB reserved per CTA.
+constexpr size_t kSmemBudgetDual = 113 * 1024;
 
 // Per-utterance descriptor, computed on the host, read by every kernel.
 struct alignas(16) UttDesc {
@@ -61,13 +64,14 @@ struct Geometry {
   int SW;         // staged symbols per frame: A (fused) or max nkey (split)
   int max_L;
   int fused;
+  int dual;       // 1: two clusters per SM pair (k_pair<K, 2>, <= kSmemBudgetDual)
   // shared-memory carve-up (bytes, 16-aligned)
   int off_xraw, off_emis, off_lse, off_el, off_occ, off_ring, off_meta, off_red;
   int ring_depth; // halo refresh ring entries per chain warp
   int off_cb;     // column buffer [2][P][cw_max] floats (TMA bulk stores / loads of lattice columns)
   int off_mbar;   // two mbarriers (one per column-buffer half)
   int off_flag;   // poisoned-frame flags: [0] this CTA's phase-1 frames, [1] written by the partner at the meet
-  int off_nrm;    // [2][column_pitch(max_L)] per-thread frame mass of each phase-2 epoch's sampled column
+  int off_nrm;    // [2][column_threads(max_L)] per-thread frame mass of each phase-2 epoch's sampled column
   int xstride;    // floats per xraw row (odd)
   int estride;    // floats per occupancy (el) row (odd)
   int cw_max;     // floats per stored column (max over batch)
@@ -96,29 +100,39 @@ inline int pick_K(int max_L) {
   return 8;
 }
 
-// Stored half-lattice column, slot-major ("transposed"): chain thread j's
-// q-th slot (q < 2K) sits at q * W + j, then one fp32 offset per chain thread
-// at 2K * W + j (forward: slot = cell s; backward: slot = s + 1). Consecutive
-// lanes touch consecutive words on every access -- the per-step stores of
-// the owning warp and the partner's phase-2 reads -- so neither has shared-
-// memory bank conflicts (the thread-major layout of round 1 gave 2K-way
-// conflicts on the partner reads, profiles/r02_bank_conflicts.txt). W has
-// one spare column so the last thread's "next thread" reads stay in the row.
-DS2CTC_HD inline int column_pitch(int L, int K) { return round_up(column_threads(L, K) + 1, 4); }
-DS2CTC_HD inline int column_offsets_base(int L, int K) { return 2 * K * column_pitch(L, K); }
-DS2CTC_HD inline int column_width(int L, int K) { return (2 * K + 1) * column_pitch(L, K); }
-// Word index of stored slot `slot` in a column of pitch W.
-DS2CTC_HD inline int column_slot(int slot, int K, int W) { return (slot % (2 * K)) * W + slot / (2 * K); }
-// Occupancy rows (phase 2): label position li of a chain thread's K label
-// cells at (li % K) * WL + li / K with WL = ceil(L / K) -- again consecutive
-// across lanes; the spare slot K * WL takes the writes of cells without a label.
-DS2CTC_HD inline int occ_pitch(int L, int K) { return (L + K - 1) / K > 0 ? (L + K - 1) / K : 1; }
-DS2CTC_HD inline int occ_index(int li, int K, int WL) { return (li % K) * WL + li / K; }
-DS2CTC_HD inline int occ_row_words(int L, int K) { return K * occ_pitch(L, K) + 1; }
+// Stored half-lattice column, warp-blocked: chain warp w owns a block of
+// (2K + 1) x 32 words; lane l's q-th slot (q < 2K) is word q * 32 + l of the
+// block and its fp32 offset word 2K * 32 + l (forward: slot = cell s;
+// backward: slot = s + 1). The strides between one lane's words are compile-
+// time (one base register + immediates per step) and consecutive lanes touch
+// consecutive words, so neither the owning warp's per-step stores nor the
+// partner's phase-2 reads have shared-memory bank conflicts (the round-1
+// thread-major layout gave 2K-way conflicts on the partner reads,
+// profiles/r02_bank_conflicts.txt). Thread j of direction d sits in warp
+// j / 28 at lane j % 28 (+ the 4 halo lanes first when d = 0, forward).
+DS2CTC_HD inline int column_block(int K) { return (2 * K + 1) * 32; }
+DS2CTC_HD inline int column_width(int L, int K) { return chain_warps_for(L, K) * column_block(K); }
+DS2CTC_HD inline int thread_lane(int j, int dir) { return j % kOwnedLanes + (dir == 0 ? kHaloLanes : 0); }
+// Word of stored slot q of chain thread j (direction dir's layout); q == 2K is its offset.
+DS2CTC_HD inline int column_word(int j, int q, int K, int dir) {
+  return (j / kOwnedLanes) * column_block(K) + q * 32 + thread_lane(j, dir);
+}
+DS2CTC_HD inline int column_slot_word(int slot, int K, int dir) { return column_word(slot / (2 * K), slot % (2 * K), K, dir); }
+// Occupancy rows (phase 2), warp-blocked the same way: lane l of chain warp w
+// writes its p-th label cell at w * K * 32 + p * 32 + l. Label position li
+// belongs to chain thread li / K, pair li % K (forward) or (li + 1) / K,
+// (li + 1) % K (backward: pair p of thread j holds label cell 2(jK + p) - 1).
+DS2CTC_HD inline int occ_row_words(int L, int K) { return chain_warps_for(L, K) * K * 32; }
+DS2CTC_HD inline int occ_word(int li, int K, int dir) {
+  const int x = dir == 0 ? li : li + 1;
+  const int j = x / K, p = x % K;
+  return (j / kOwnedLanes) * K * 32 + p * 32 + thread_lane(j, dir);
+}
 
 // max_L_all: the longest label of the whole batch (it fixes K and hence the
 // stored column layout, see make_layout); max_L: the longest that runs.
-inline Geometry make_geometry(int max_L_all, int max_L, int max_nkey, int A, bool fused) {
+inline Geometry make_geometry(int max_L_all, int max_L, int max_nkey, int A, bool fused,
+                              size_t budget = kSmemBudget) {
   Geometry g{};
   g.K = pick_K(max_L_all);
   g.nchain = chain_warps_for(max_L, g.K);
@@ -148,14 +162,14 @@ inline Geometry make_geometry(int max_L_all, int max_L, int max_nkey, int A, boo
     g.off_ring = take(8 * g.nchain * g.ring_depth * kHaloLanes * (2 * g.K + 1));
     g.off_cb = take(4 * 2 * P * g.cw_max);
     g.off_mbar = take(16);
-    g.off_nrm = take(4 * 2 * column_pitch(max_L, g.K));
+    g.off_nrm = take(4 * 2 * column_threads(max_L, g.K));
     // meta: labels (L+1), key_char (nkey), key_start (nkey+1), key_pos (L), slot of each label
     // position (L+1), symbol -> slot (A shorts, fused)
     g.off_meta = take(4 * (4 * max_L + 2 * max_nkey + 8) + (fused ? 2 * A : 0));
-    g.off_red = take(8 * 72);
+    g.off_red = take(2048);  // meet reductions (doubles per warp) and the drain's per-part totals (floats)
     g.off_flag = take(16);
     g.smem = off;
-    if (static_cast<size_t>(off) <= kSmemBudget) break;
+    if (static_cast<size_t>(off) <= budget) break;
   }
   return g;
 }

@@ -89,6 +89,18 @@ def run(so, A=29, T=700, L=150, B=64, brief=False):
                   f"tail {meetbuf[16 + cta] - m[7]}, total {meetbuf[16 + cta] - m[6]}")
             print(f"  cta{cta}: meet: store+wait {m[1]-m[0]}, cluster barrier {m[2]-m[1]}, logZ {m[3]-m[2]}, "
                   f"shift+load {m[4]-m[3]}, sync {m[5]-m[4]}")
+    pro = np.zeros((2, 8, 8), dtype=np.int64)
+    if hasattr(lib, "ds2ctc_debug_prologue_clocks") and \
+            lib.ds2ctc_debug_prologue_clocks(pro.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong))) == 0:
+        meetbuf2 = np.zeros(18, dtype=np.int64)
+        lib.ds2ctc_debug_meet_clocks(meetbuf2.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong)))
+        for cta in range(2):
+            start = meetbuf2[cta * 8 + 6]
+            rows = []
+            for pt in range(5):
+                v = [int(pro[cta, pt, w] - start) if pro[cta, pt, w] else None for w in range(6)]
+                rows.append(f"p{pt}:" + ",".join("-" if x is None else str(x) for x in v))
+            print(f"  cta{cta}: prologue stamps (per warp 0..5, from kernel start) " + "  ".join(rows))
     if brief:
         for cta in range(2):
             rows = [buf[cta, e] for e in range(128) if buf[cta, e, 0, 0] != 0]
