@@ -53,6 +53,12 @@ WORKLOADS = {
                       desc="SortaGrad batch T~U[50,1500] L~U[5,min(300,T/2)] B=512 sharded over N GPUs"),
     "edge1500": dict(A=29, T=1500, L=300, total=1024, scaling="strong",
                      desc="B=1024 at T=1500 L=300 sharded over N GPUs"),
+    # the CTC step plus its gradient's consumer, the output
+    # FC backward (nn.cpp:874-899) on tcgen05, on the device-resident gradient,
+    # and for N > 1 the parameter-gradient all-reduce (trainer.cpp:175) over NCCL
+    "english-step": dict(A=29, T=700, L=150, per_gpu=64, fc_hidden=2560, scaling="weak",
+                         desc="English DS2 shape + output-FC backward (H=2560, the paper's 2560-unit "
+                              "model) on the device-resident CTC gradient, 64 utterances per GPU"),
 }
 
 
@@ -300,12 +306,41 @@ def main():
                 print(f"peer all-reduce unavailable ({peer.error}); using NCCL", file=sys.stderr)
             peer = None
 
+    # f1: the output layer's cached input, weight and parameter gradients (random init)
+    H = wl.get("fc_hidden", 0)
+    if H:
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(4321 + rank)
+        fc_x = torch.randn((x.shape[0], B, H), generator=gen, device=dev, dtype=torch.float32)
+        fc_w = torch.randn((A, H), generator=gen, device=dev, dtype=torch.float32) * 0.02
+        fc_dw = torch.zeros((A, H), device=dev, dtype=torch.float32)
+        fc_db = torch.zeros(A, device=dev, dtype=torch.float32)
+        fc_dx = torch.empty((x.shape[0], B, H), device=dev, dtype=torch.float32)
+        fc_ws = ctc.Workspace(dev)
+        fc_sz = ctypes.c_size_t()
+        _lib.check(lib.ds2ctc_fc_backward_workspace_size(x.shape[0] * B, A, H, ctypes.byref(fc_sz)), "fc ws")
+        fc_ws_ptr, fc_ws_bytes = fc_ws.get(int(fc_sz.value))
+
+    def fc_step():
+        fc_dw.zero_()  # zero_grads (trainer.cpp:152)
+        fc_db.zero_()
+        _lib.check(lib.ds2ctc_fc_backward(ctypes.c_void_p(grads.data_ptr()), ctypes.c_void_p(fc_x.data_ptr()),
+                                          ctypes.c_void_p(fc_w.data_ptr()), ctypes.c_void_p(fc_dw.data_ptr()),
+                                          ctypes.c_void_p(fc_db.data_ptr()), ctypes.c_void_p(fc_dx.data_ptr()),
+                                          x.shape[0] * B, A, H, ctypes.c_void_p(fc_ws_ptr), fc_ws_bytes,
+                                          ctypes.c_void_p(stream.cuda_stream)), "ds2ctc_fc_backward")
+        if world > 1:  # f4: the parameter-gradient all-reduce (trainer.cpp:175, ring_allreduce -> NCCL)
+            dist.all_reduce(fc_dw)
+            dist.all_reduce(fc_db)
+
     def step(reduce_mode=None):
         st = lib.ds2ctc_compute_loss_checked(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(grads.data_ptr()),
                                              lab_c.ctypes.data_as(P), ll_c.ctypes.data_as(P),
                                              il_c.ctypes.data_as(P), A, B, A - 1, ctypes.c_void_p(costs.data_ptr()),
                                              ctypes.c_void_p(ws_ptr), ws_bytes, ctypes.c_void_p(stream.cuda_stream))
         _lib.check(st, "ds2ctc_compute_loss")
+        if H:
+            fc_step()
         if peer is not None and reduce_mode != "nccl":
             peer.reduce(costs.data_ptr(), B, pair.data_ptr(), stream.cuda_stream)
             return
@@ -324,7 +359,7 @@ def main():
 
     # kernels of ours per step: k_pair (+ k_dense + k_finalize for large A) + k_loss_sum / k_loss_allreduce
     if B:
-        launches_per_step = 1 + (2 if A > 128 else 0) + 1
+        launches_per_step = 1 + (2 if A > 128 else 0) + 1 + (5 if H else 0)  # fc: pad, bias, W^T, 2 GEMMs
     else:
         launches_per_step = 1
 

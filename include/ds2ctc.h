@@ -227,6 +227,29 @@ ds2ctc_status ds2ctc_profile_read(int call_index, float* ms);
  */
 ds2ctc_status ds2ctc_debug_watchdog(unsigned long long* out4);
 
+/*
+ * The CTC gradient's consumer: the output fully connected
+ * layer's backward pass, FullyConnectedLayer::backward (proj/src/nn.cpp:874-899)
+ * for the output layer built by network.cpp:135 (no ReLU, no batch norm), on
+ * tcgen05 tensor cores (tf32 inputs, fp32 accumulation) with the gradient
+ * still on the device:
+ *   db[A]    += sum_r dlogits[r][:]          (nn.cpp:886-890)
+ *   dw[A][H] += dlogits^T x                  (matmul_tn, nn.cpp:894)
+ *   dx[r][H]  = dlogits w                    (matmul, nn.cpp:895)
+ * dlogits is DEVICE fp32 [rows][out_dim] -- the gradients buffer of
+ * ds2ctc_compute_loss viewed as rows = T_max * minibatch (padded frames are
+ * zero rows); x DEVICE fp32 [rows][in_dim] (the layer's input, same row
+ * order); w DEVICE fp32 [out_dim][in_dim]; dw / db accumulate (the caller
+ * zeroes them per step, like zero_grads, trainer.cpp:152); dx is written;
+ * dw, db, dx are each nullable. in_dim must be a multiple of 4 and the
+ * buffers 16-byte aligned (TMA). The workspace (ds2ctc_fc_backward_workspace_size)
+ * re-pitches the gradient rows when out_dim % 4 != 0. Asynchronous on `stream`.
+ * Tolerance vs the fp64 reference: tf32 products (10-bit mantissa), fp32 sums.
+ */
+ds2ctc_status ds2ctc_fc_backward_workspace_size(int rows, int out_dim, int in_dim, size_t* bytes);
+ds2ctc_status ds2ctc_fc_backward(const float* dlogits, const float* x, const float* w, float* dw, float* db, float* dx,
+                                 int rows, int out_dim, int in_dim, void* workspace, size_t workspace_bytes,
+                                 void* stream);
 /* ---------------------------------------------------------------------
  * H1 host scheduler (trainer.cpp:58-91, 140-143) -- pure host functions.
  * ------------------------------------------------------------------- */

@@ -98,6 +98,9 @@ def ref_lib():
         lib.ref_sortagrad_order.restype = None
         lib.ref_sortagrad_order.argtypes = [_c_int_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_uint64,
                                             ctypes.c_int, _c_i64_p]
+        lib.ref_fc_backward.restype = None
+        lib.ref_fc_backward.argtypes = [_c_float_p, _c_float_p, _c_int_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                        ctypes.c_int, _c_float_p, _c_double_p, _c_double_p, _c_double_p]
         lib.ref_ctc_batch.restype = None
         lib.ref_ctc_batch.argtypes = [_c_float_p, _c_int_p, _c_int_p, _c_int_p, ctypes.c_int, ctypes.c_int,
                                       ctypes.c_int, _c_double_p, _c_float_p, ctypes.c_int]
@@ -244,3 +247,21 @@ def oracle_sortagrad(lengths, global_batch, epoch, seed, sortagrad_on=True):
 
 def ref_sortagrad(lengths, global_batch, epoch, seed, sortagrad_on=True):
     return _sortagrad(ref_lib().ref_sortagrad_order, lengths, global_batch, epoch, seed, sortagrad_on)
+
+
+def ref_fc_backward(x, dlogits, input_lengths, w):
+    """The reference's output-layer backward (asr::nn FullyConnectedLayer, nn.cpp:874-899) on
+    batched [T_max][B][H] inputs and [T_max][B][A] gradients -> (dw A x H, db A, dx [T_max][B][H]), fp64."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    g = np.ascontiguousarray(dlogits, dtype=np.float32)
+    w = np.ascontiguousarray(w, dtype=np.float32)
+    il = np.ascontiguousarray(input_lengths, dtype=np.int32)
+    Tmax, B, H = x.shape
+    A = g.shape[2]
+    dw = np.zeros((A, H), np.float64)
+    db = np.zeros(A, np.float64)
+    dx = np.zeros((Tmax, B, H), np.float64)
+    ref_lib().ref_fc_backward(_ptr(x, _c_float_p), _ptr(g, _c_float_p), _ptr(il, _c_int_p), B, Tmax, H, A,
+                              _ptr(w, _c_float_p), _ptr(dw, _c_double_p), _ptr(db, _c_double_p),
+                              _ptr(dx, _c_double_p))
+    return dw, db, dx

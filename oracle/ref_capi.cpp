@@ -18,6 +18,7 @@
 
 #include "asr/common.hpp"
 #include "asr/ctc.hpp"
+#include "asr/nn.hpp"
 #include "asr/trainer.hpp"
 
 using asr::Matrix;
@@ -142,6 +143,44 @@ void ref_ctc_batch(const float* acts, const int* flat_labels, const int* label_l
     for (int i = 0; i < nthreads; ++i) th.emplace_back(body);
     for (auto& t : th) t.join();
   }
+}
+
+// The reference's own output-layer backward: asr::nn::make_fully_connected(H, A,
+// relu = false, batchnorm = false) (network.cpp:135), train-mode forward on the
+// utterance matrices x[b] (T_b x H) to cache them, then backward(dlogits[b])
+// (nn.cpp:874-899). Inputs are the batched [T_max][B][.] buffers; w is A x H.
+// Outputs: dw (A x H), db (A), dx [T_max][B][H] (zero past T_b). fp64 throughout.
+void ref_fc_backward(const float* x, const float* dlogits, const int* input_lengths, int B, int Tmax, int H, int A,
+                     const float* w, double* dw, double* db, double* dx) {
+  auto layer = asr::nn::make_fully_connected(H, A, false, false);
+  std::vector<asr::nn::ParamRef> params;
+  layer->collect("fc", params);
+  for (auto& p : params) {
+    if (p.value->rows() == A && p.value->cols() == H)
+      for (int i = 0; i < A * H; ++i) p.value->data()[i] = w[i];
+  }
+  asr::nn::Batch in(B), dout(B);
+  for (int b = 0; b < B; ++b) {
+    const int T = input_lengths[b];
+    in[b] = Matrix(T, H);
+    dout[b] = Matrix(T, A);
+    for (int t = 0; t < T; ++t) {
+      for (int h = 0; h < H; ++h) in[b](t, h) = x[(static_cast<size_t>(t) * B + b) * H + h];
+      for (int a = 0; a < A; ++a) dout[b](t, a) = dlogits[(static_cast<size_t>(t) * B + b) * A + a];
+    }
+  }
+  layer->forward(in, /*train=*/true);
+  asr::nn::Batch dxb = layer->backward(dout);
+  for (auto& p : params) {
+    if (p.grad->rows() == A && p.grad->cols() == H)
+      for (int i = 0; i < A * H; ++i) dw[i] = p.grad->data()[i];
+    else if (p.grad->rows() == 1 && p.grad->cols() == A)
+      for (int i = 0; i < A; ++i) db[i] = p.grad->data()[i];
+  }
+  for (int t = 0; t < Tmax; ++t)
+    for (int b = 0; b < B; ++b)
+      for (int h = 0; h < H; ++h)
+        dx[(static_cast<size_t>(t) * B + b) * H + h] = t < input_lengths[b] ? dxb[b](t, h) : 0.0;
 }
 
 }  // extern "C"

@@ -36,6 +36,8 @@ EXPORTS = (
     "ds2ctc_mailbox_close",
     "ds2ctc_loss_sum_allreduce",
     "ds2ctc_reduce_fault",
+    "ds2ctc_fc_backward_workspace_size",
+    "ds2ctc_fc_backward",
     "ds2ctc_viterbi_get_workspace_size",
     "ds2ctc_viterbi_align",
     "ds2ctc_lattice_get_sizes",
@@ -120,6 +122,11 @@ def lib():
             L.ds2ctc_loss_sum_allreduce.restype = ctypes.c_int
             L.ds2ctc_loss_sum_allreduce.argtypes = [_p, ctypes.c_int, _p, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int,
                                                     ctypes.c_int, ctypes.c_ulonglong, _p]
+            L.ds2ctc_fc_backward_workspace_size.restype = ctypes.c_int
+            L.ds2ctc_fc_backward_workspace_size.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _szp]
+            L.ds2ctc_fc_backward.restype = ctypes.c_int
+            L.ds2ctc_fc_backward.argtypes = [_p, _p, _p, _p, _p, _p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p,
+                                             ctypes.c_size_t, _p]
             L.ds2ctc_reduce_fault.restype = ctypes.c_int
             L.ds2ctc_reduce_fault.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
             L.ds2ctc_viterbi_get_workspace_size.restype = ctypes.c_int

@@ -22,7 +22,8 @@ LIB = os.path.join(PKG, "libds2ctc.so")
 BUILD = os.path.join(PKG, "_build")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["ctc_pair.cu", "ctc_pair_k8.cu", "ctc_dense.cu", "ctc_viterbi.cu", "ctc_lattice.cu", "ctc_reduce.cu"]
+CU_SOURCES = ["ctc_pair.cu", "ctc_pair_k8.cu", "ctc_dense.cu", "ctc_viterbi.cu", "ctc_lattice.cu", "ctc_reduce.cu",
+              "fc_backward.cu"]
 # Per-source extra flags. ctc_pair_k8.cu: ptxas 12.9 -O3 segfaults on the
 # K = 8 pair kernel at its 168-register budget; -O1 builds it without spills.
 CU_FLAGS = {"ctc_pair_k8.cu": ["-Xptxas", "-O1"]}

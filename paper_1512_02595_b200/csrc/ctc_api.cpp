@@ -803,6 +803,33 @@ ds2ctc_status ds2ctc_loss_sum(const float* costs, int minibatch, double* out2, v
   return DS2CTC_STATUS_SUCCESS;
 }
 
+ds2ctc_status ds2ctc_fc_backward_workspace_size(int rows, int out_dim, int in_dim, size_t* bytes) {
+  if (bytes == nullptr || rows < 0 || out_dim < 1 || in_dim < 1) return DS2CTC_STATUS_INVALID_VALUE;
+  *bytes = fc_backward_workspace(rows, out_dim, in_dim);
+  return DS2CTC_STATUS_SUCCESS;
+}
+
+ds2ctc_status ds2ctc_fc_backward(const float* dlogits, const float* x, const float* w, float* dw, float* db, float* dx,
+                                 int rows, int out_dim, int in_dim, void* workspace, size_t workspace_bytes,
+                                 void* stream) {
+  if (rows < 0 || out_dim < 1 || in_dim < 1) return DS2CTC_STATUS_INVALID_VALUE;
+  if (rows == 0) return DS2CTC_STATUS_SUCCESS;
+  if (dlogits == nullptr || (dw != nullptr && x == nullptr) || (dx != nullptr && w == nullptr))
+    return DS2CTC_STATUS_INVALID_VALUE;
+  // TMA: 16-byte aligned bases and row pitches (in_dim % 4 == 0); the gradient
+  // rows are re-pitched into the workspace when out_dim % 4 != 0
+  if (in_dim % 4 != 0) return DS2CTC_STATUS_UNSUPPORTED;
+  for (const void* p : {static_cast<const void*>(dlogits), static_cast<const void*>(x), static_cast<const void*>(w),
+                        static_cast<const void*>(dx)})
+    if (p != nullptr && reinterpret_cast<uintptr_t>(p) % 16 != 0) return DS2CTC_STATUS_INVALID_VALUE;
+  const size_t need = fc_backward_workspace(rows, out_dim, in_dim);
+  if (workspace_bytes < need || (need > 0 && (workspace == nullptr || reinterpret_cast<uintptr_t>(workspace) % 256)))
+    return DS2CTC_STATUS_INVALID_VALUE;
+  if (fc_backward(dlogits, x, w, dw, db, dx, rows, out_dim, in_dim, workspace, sm_count(), stream) != cudaSuccess)
+    return DS2CTC_STATUS_EXECUTION_FAILED;
+  return DS2CTC_STATUS_SUCCESS;
+}
+
 ds2ctc_status ds2ctc_profile_enable(int slots) {
   if (slots < 0) return DS2CTC_STATUS_INVALID_VALUE;
   Profiler& p = profiler();

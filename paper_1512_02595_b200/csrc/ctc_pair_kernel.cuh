@@ -46,6 +46,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "ds2ctc_internal.h"
 
@@ -404,16 +405,10 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   __syncthreads();
   PRO_STAMP(1);
   auto frame = [&](int k) { return dir == 0 ? k : T - 1 - k; };
-  // Phase-2 epoch lengths: P, except that the last two epochs are Q = P / 4
-  // frames each -- after the loop the gradient warp still has to sum and write
-  // the last epoch's rows and the service warp the one before (the drain),
-  // which costs ~Q / P of a full epoch's helper work instead of all of it.
-  auto phase2_len = [&](int rem) {
-    const int Q = P >= 8 ? P / 4 : P;
-    if (rem <= Q) return rem;
-    if (rem <= 2 * Q) return rem - Q;
-    return min(P, rem - 2 * Q);
-  };
+  // Phase-2 epochs are P frames. (Shorter final epochs to shrink the drain
+  // were measured slower: the gradient warp's label sums cost ~L per epoch
+  // whatever its length, so each extra epoch costs a full helper epoch.)
+  auto phase2_len = [&](int rem) { return min(P, rem); };
   auto next_epoch = [&](const Epoch& e) -> Epoch {
     if (e.phase == 1) {
       if (e.k1 <= kmid) return {e.k1, min(e.k1 + P, kmid + 1), 1};
@@ -942,7 +937,8 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   // `full` (the epoch's last column only): the blank cells too, and this
   // thread's share of sum_s 2^gamma(s, t) for the gradient warp's per-frame
   // renormalisation (grad_occ).
-  auto occupancy_column = [&](int k, const Epoch& e, bool full) {
+  auto occupancy_column = [&](int k, const Epoch& e, auto full_tag) {
+    constexpr bool full = decltype(full_tag)::value;  // compile-time: the hot loop's copy has no blank-cell code
 #ifdef DS2CTC_EXP_NOOCC
     return;
 #endif
@@ -950,7 +946,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     float d[K];
 #pragma unroll
     for (int p = 0; p < K; ++p) d[p] = pd[p];
-    if (!full) partner_fetch(min(k + 1, e.k1 - 1), e);
+    if constexpr (!full) partner_fetch(min(k + 1, e.k1 - 1), e);
     float* elr = el + (k & M2) * g.estride;
     float tot = 0.f;
 #pragma unroll
@@ -961,7 +957,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
       const float ml = ex2(ol + (rl + d[p]));
       elr[el_base + p * 32] = ml;
 #ifndef DS2CTC_EXP_NOFRAMEMASS
-      if (full) {
+      if constexpr (full) {
         // blank 2i: forward partner slot 2i + 1, backward partner slot 2i (both thread ctid)
         const float* row = cb_row(k, e);
         const float rb = dir == 0 ? vb[p] : xb[p];
@@ -971,7 +967,9 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
 #endif
     }
 #ifndef DS2CTC_EXP_NOFRAMEMASS
-    if (full && stores) nrm[(ep & 1) * NPW + ctid] = tot;
+    if constexpr (full) {
+      if (stores) nrm[(ep & 1) * NPW + ctid] = tot;
+    }
 #endif
   };
 
@@ -1008,7 +1006,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
         for (; k < kb; ++k) {
           STEP_STAMP(k, e, 0);
           const Nb nb = neighbour(k);
-          occupancy_column(k - 1, e, false);
+          occupancy_column(k - 1, e, std::false_type{});
           step(k, nb);
           load_emis(k + 1);
           STEP_STAMP(k, e, 2);
@@ -1029,7 +1027,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
       }
     }
     if (ph2) {
-      occupancy_column(e.k1 - 1, e, true);
+      occupancy_column(e.k1 - 1, e, std::true_type{});
     } else {
       store_column(e.k1 - 1, e);
       fence_async_shared();  // the service warp bulk-stores this epoch's columns

@@ -322,6 +322,10 @@ size_t mailbox_bytes(int world);
 int read_reduce_fault(unsigned long long* seq);
 int read_watchdog(unsigned long long* out4);
 size_t viterbi_smem_bytes(int T, int L);
+// Output-FC backward on tcgen05 (fc_backward.cu; nn.cpp:874-899).
+size_t fc_backward_workspace(int rows, int A, int H);
+int fc_backward(const float* g, const float* x, const float* w, float* dw, float* db, float* dx, int rows, int A,
+                int H, void* workspace, int sm_count, void* stream);
 int launch_viterbi(const ViterbiArgs& a, size_t smem, void* stream);
 size_t lattice_smem_bytes(int T, int L);
 int launch_lattice(const LatticeArgs& a, size_t smem, void* stream);

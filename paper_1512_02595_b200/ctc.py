@@ -267,3 +267,44 @@ def ctc_lattice(frame_logits, label: Sequence[int], blank: int, device: int = 0)
     for c in lab:
         aug += [c, blank]
     return CtcLattice(aug, alpha.cpu().numpy().reshape(S, T), beta.cpu().numpy().reshape(S, T), float(lp[0].item()))
+
+
+def fc_backward(dlogits, x, w, dw=None, db=None, dx=None, want_dx: bool = True, stream=None,
+                workspace: Optional[Workspace] = None):
+    """The output layer's backward pass on the CTC gradient, on the device
+    (ds2ctc_fc_backward; FullyConnectedLayer::backward, nn.cpp:874-899):
+    db += sum_rows dlogits, dw += dlogits^T x, dx = dlogits w.
+
+    dlogits: float32 CUDA [T, B, A] (the compute_ctc_loss gradients), x: float32
+    CUDA [T, B, H], w: float32 CUDA [A, H]. dw [A, H] / db [A] accumulate (zeros
+    when not given). Returns (dw, db, dx or None); asynchronous on `stream`."""
+    import torch
+
+    for t in (dlogits, x, w):
+        if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+            raise ValueError("dlogits, x, w must be contiguous float32 CUDA tensors")
+    T, B, A = dlogits.shape
+    H = x.shape[-1]
+    if x.shape[:2] != (T, B) or tuple(w.shape) != (A, H):
+        raise ValueError("shapes: dlogits [T,B,A], x [T,B,H], w [A,H]")
+    dev = dlogits.device
+    dw = torch.zeros((A, H), dtype=torch.float32, device=dev) if dw is None else dw
+    db = torch.zeros(A, dtype=torch.float32, device=dev) if db is None else db
+    if want_dx and dx is None:
+        dx = torch.empty((T, B, H), dtype=torch.float32, device=dev)
+    rows = T * B
+    out = ctypes.c_size_t()
+    _lib.check(_lib.lib().ds2ctc_fc_backward_workspace_size(rows, A, H, ctypes.byref(out)),
+               "ds2ctc_fc_backward_workspace_size")
+    if workspace is None:
+        workspace = _default_ws.setdefault(("fc", dev.index), Workspace(dev))
+    ws_ptr, ws_bytes = workspace.get(int(out.value))
+    if stream is None:
+        stream = torch.cuda.current_stream(dev)
+    st = _lib.lib().ds2ctc_fc_backward(
+        ctypes.c_void_p(dlogits.data_ptr()), ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(w.data_ptr()),
+        ctypes.c_void_p(dw.data_ptr()), ctypes.c_void_p(db.data_ptr()),
+        ctypes.c_void_p(dx.data_ptr()) if want_dx else None, rows, A, H, ctypes.c_void_p(ws_ptr), ws_bytes,
+        ctypes.c_void_p(stream.cuda_stream))
+    _lib.check(st, "ds2ctc_fc_backward")
+    return dw, db, (dx if want_dx else None)
