@@ -431,17 +431,27 @@ def main():
         _lib.check(lib.ds2ctc_profile_read(k, ms4), "ds2ctc_profile_read")
         stage[k] = list(ms4)
     lib.ds2ctc_profile_enable(0)
+    fc_ms_local = 0.0
+    if H:  # the FC backward alone (events on the launching stream), L2 flushed before each
+        fe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_prof)]
+        for k in range(n_prof):
+            flush.zero_()
+            fe[k][0].record(stream)
+            fc_step()
+            fe[k][1].record(stream)
+        torch.cuda.synchronize()
+        fc_ms_local = statistics.mean(a.elapsed_time(b) for a, b in fe)
     ms_local = statistics.mean(step_ms)
     pair_ms_local = float(stage[:, 0].mean()) if B else 0.0
     dense_ms_local = float(stage[:, 1].mean()) if B else 0.0
     final_ms_local = float(stage[:, 2].mean()) if B else 0.0
 
     # ---- max over ranks ----
-    vals = torch.tensor([ms_local, pair_ms_local, e2e_ms_local, dense_ms_local, final_ms_local],
+    vals = torch.tensor([ms_local, pair_ms_local, e2e_ms_local, dense_ms_local, final_ms_local, fc_ms_local],
                         dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-    ms, pair_ms, e2e_ms, dense_ms, final_ms = [float(v) for v in vals.cpu()]
+    ms, pair_ms, e2e_ms, dense_ms, final_ms, fc_ms = [float(v) for v in vals.cpu()]
     total_utts = int(il_g.shape[0])
     total_frames = int(il_g.sum())
     value = total_utts / (ms / 1e3)
@@ -524,6 +534,18 @@ def main():
             "clocks": clocks,
             "loss_sum": loss_sum, "skipped": int(skipped),
         }
+        if H:
+            # f1: the FC backward is HBM-bound at A = 29 (K = 29 for dx): x read once for
+            # dW, dx written once, the gradient read twice, W / W^T / dW negligible
+            rows = x.shape[0] * B
+            fc_bytes = 4.0 * (2 * rows * H + 2 * rows * A + 3 * A * H)
+            fc_flops = 2.0 * 2 * rows * A * H
+            line["fc_backward"] = {"ms": fc_ms, "rows": rows, "in_dim": H, "out_dim": A, "alg_bytes": fc_bytes,
+                                   "achieved_gbs": fc_bytes / (fc_ms / 1e3) / 1e9 if fc_ms else None,
+                                   "frac_hbm": fc_bytes / (fc_ms / 1e3) / 1e9 / peak if fc_ms else None,
+                                   "tflops": fc_flops / (fc_ms / 1e3) / 1e12 if fc_ms else None,
+                                   "kernels": "tcgen05 kind::tf32 (k_fc_gemm x2) + bias sum + W^T + row pad",
+                                   "param_grad_allreduce": "nccl all_reduce (dW, db)" if world > 1 else "none"}
         if world == 1 and not args.no_cpu_baseline:
             # The reference CPU CTC on the same inputs: (i) all host cores, one
             # utterance per thread (the paper's CPU CTC); (ii) one

@@ -243,6 +243,34 @@ std::pair<int, int> build_metadata(const Layout& lay, const int* flat_labels, co
   return {max_L, max_nkey};
 }
 
+// DS2CTC_DENSE_OVERLAP=0: the large-alphabet HBM pass after k_pair (one
+// kernel) instead of concurrently with it (default on).
+bool dense_overlap_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("DS2CTC_DENSE_OVERLAP");
+    return v == nullptr || std::atoi(v) != 0;
+  }();
+  return on;
+}
+
+struct OverlapStreams {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  bool init() {
+    if (side) return true;
+    return cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) == cudaSuccess &&
+           cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&join, cudaEventDisableTiming) == cudaSuccess;
+  }
+};
+
+OverlapStreams& overlap_streams_for_current_device() {
+  thread_local std::map<int, OverlapStreams> per_device;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return per_device[dev];
+}
+
 int sm_count() {
   static int n[64] = {};
   int dev = 0;
@@ -334,9 +362,28 @@ ds2ctc_status run(const float* acts, float* grads, const int* flat_labels, const
   Profiler& prof = profiler();
   const bool timed = !prof.suspended && prof.ready(dev);
   if (timed) prof.mark(0, s);
+  // Large alphabets: the dense softmax pass (k_dense_soft, HBM-bound) needs
+  // nothing from k_pair (latency-bound, HBM idle), so it runs on a forked
+  // stream concurrently with it; the key-column patch follows both.
+  OverlapStreams* ov = nullptr;
+  if (!fused && dense_overlap_enabled()) {
+    ov = &overlap_streams_for_current_device();
+    if (!ov->init() || cudaEventRecord(ov->fork, s) != cudaSuccess ||
+        cudaStreamWaitEvent(ov->side, ov->fork, 0) != cudaSuccess)
+      return DS2CTC_STATUS_EXECUTION_FAILED;
+  }
   if (launch_pair(a, stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
   if (timed) prof.mark(1, s);
-  if (!fused && launch_dense(a, grads != nullptr, stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  if (ov != nullptr) {
+    const bool ok = launch_dense_soft(a, grads != nullptr, ov->side) == cudaSuccess;
+    // the caller's stream waits for the side stream on every path (ordering)
+    if (cudaEventRecord(ov->join, ov->side) != cudaSuccess || cudaStreamWaitEvent(s, ov->join, 0) != cudaSuccess ||
+        !ok)
+      return DS2CTC_STATUS_EXECUTION_FAILED;
+    if (launch_dense_patch(a, stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  } else if (!fused && launch_dense(a, grads != nullptr, stream) != cudaSuccess) {
+    return DS2CTC_STATUS_EXECUTION_FAILED;
+  }
   if (timed) prof.mark(2, s);
   if (!fused && launch_finalize(a, stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
   if (timed) {

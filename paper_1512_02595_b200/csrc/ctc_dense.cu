@@ -146,6 +146,96 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense(PairArgs a, int write_g
   }
 }
 
+// The HBM pass split in two so that its bulk overlaps k_pair (which leaves the
+// memory system idle for ~110 us at the Mandarin shape, while its one CTA
+// per SM leaves room for more):
+//  k_dense_soft  -- needs nothing from k_pair: per (t, b) row the max and the
+//                   log-sum-exp (log_softmax_rows, ctc.cpp:24-37) and the
+//                   softmax row written to the gradient, exp evaluated once
+//                   per element (kept in registers between the sum and the
+//                   store). Runs on a forked stream concurrently with k_pair.
+//  k_dense_patch -- after k_pair: subtract the occupancies at the <= L + 1
+//                   key columns of each row (grad_column, ctc.cpp:69-79), and
+//                   zero the rows of utterances whose lattice has no mass.
+__global__ void __launch_bounds__(kDenseThreads) k_dense_soft(PairArgs a, int write_grad) {
+  __shared__ float sh[32];
+  const int row = blockIdx.x;
+  const int t = row / a.B;
+  const int b = row - t * a.B;
+  const UttDesc u = a.desc[b];
+  const int A = a.A;
+  const int tid = threadIdx.x;
+  float* gr = write_grad ? a.grad + static_cast<size_t>(row) * A : nullptr;
+  const float* xr = a.x + static_cast<size_t>(row) * A;
+  if (!(u.status == 0 && t < u.T)) {
+    if (gr)
+      for (int c = tid; c < A; c += kDenseThreads) gr[c] = 0.f;
+    return;
+  }
+  const bool vec = (A & 3) == 0 && A <= kDenseVec * kDenseThreads * 4;
+  float m, ls;
+  if (vec) {  // the row stays in registers: one HBM read, one HBM write
+    const int n4 = A >> 2;
+    const float4* x4 = reinterpret_cast<const float4*>(xr);
+    float4 v[kDenseVec];
+    m = -__builtin_huge_valf();
+#pragma unroll
+    for (int j = 0; j < kDenseVec; ++j) {
+      const int q = tid + j * kDenseThreads;
+      v[j] = q < n4 ? ldg_stream(x4 + q) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      m = fmaxf(m, fmaxf(fmaxf(v[j].x, v[j].y), fmaxf(v[j].z, v[j].w)));
+    }
+    m = block_max(m, sh);
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < kDenseVec; ++j) {
+      v[j] = make_float4(__expf(v[j].x - m), __expf(v[j].y - m), __expf(v[j].z - m), __expf(v[j].w - m));
+      s += (v[j].x + v[j].y) + (v[j].z + v[j].w);
+    }
+    s = block_sum(s, sh);
+    ls = logf(s);
+    if (gr) {
+      float4* g4 = reinterpret_cast<float4*>(gr);
+      const float inv = 1.f / s;
+#pragma unroll
+      for (int j = 0; j < kDenseVec; ++j) {
+        const int q = tid + j * kDenseThreads;
+        if (q < n4) stg_stream(g4 + q, make_float4(v[j].x * inv, v[j].y * inv, v[j].z * inv, v[j].w * inv));
+      }
+    }
+  } else {  // generic: two passes (the second hits L1/L2)
+    m = -__builtin_huge_valf();
+    for (int c = tid; c < A; c += kDenseThreads) m = fmaxf(m, __ldg(xr + c));
+    m = block_max(m, sh);
+    float s = 0.f;
+    for (int c = tid; c < A; c += kDenseThreads) s += __expf(__ldg(xr + c) - m);
+    s = block_sum(s, sh);
+    ls = logf(s);
+    if (gr)
+      for (int c = tid; c < A; c += kDenseThreads) gr[c] = __expf(__ldg(xr + c) - (m + ls));
+  }
+  if (tid == 0) a.lse[row] = make_float2(m, ls);
+}
+
+// One warp per (t, b) row.
+__global__ void k_dense_patch(PairArgs a) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= a.t_max * a.B) return;
+  const int t = row / a.B;
+  const int b = row - t * a.B;
+  const UttDesc u = a.desc[b];
+  if (!(u.status == 0 && t < u.T)) return;  // zero rows written by k_dense_soft
+  float* gr = a.grad + static_cast<size_t>(row) * a.A;
+  if (a.logz[b] == -__builtin_huge_val()) {  // no path has mass (ctc.cpp:189-193): zero gradient
+    for (int c = lane; c < a.A; c += 32) gr[c] = 0.f;
+    return;
+  }
+  const int* keys = a.key_char + u.key_off;
+  const float* occ = a.occ + u.occ_off + static_cast<size_t>(t) * u.nkey;
+  for (int j = lane; j < u.nkey; j += 32) gr[keys[j]] -= occ[j];
+}
+
 // costs[b] = sum_t lse_t - log Z (natural log), one warp per utterance.
 // log Z = log Z' + sum_t mk_t, with log Z' (log2 units) from k_pair.
 __global__ void k_finalize(PairArgs a) {
@@ -208,6 +298,21 @@ int launch_dense(const PairArgs& a, bool write_grad, void* stream) {
   const long long rows = static_cast<long long>(a.t_max) * a.B;
   if (rows == 0) return cudaSuccess;
   k_dense<<<static_cast<unsigned>(rows), kDenseThreads, 0, static_cast<cudaStream_t>(stream)>>>(a, write_grad ? 1 : 0);
+  return cudaGetLastError();
+}
+
+int launch_dense_soft(const PairArgs& a, bool write_grad, void* stream) {
+  const long long rows = static_cast<long long>(a.t_max) * a.B;
+  if (rows == 0) return cudaSuccess;
+  k_dense_soft<<<static_cast<unsigned>(rows), kDenseThreads, 0, static_cast<cudaStream_t>(stream)>>>(a,
+                                                                                                    write_grad ? 1 : 0);
+  return cudaGetLastError();
+}
+
+int launch_dense_patch(const PairArgs& a, void* stream) {
+  const long long rows = static_cast<long long>(a.t_max) * a.B;
+  if (rows == 0 || a.grad == nullptr) return cudaSuccess;
+  k_dense_patch<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
   return cudaGetLastError();
 }
 

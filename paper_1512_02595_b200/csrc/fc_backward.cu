@@ -25,6 +25,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <utility>
 #include <cstdint>
 
 #include "ds2ctc_internal.h"
@@ -33,11 +34,10 @@ namespace ds2ctc {
 namespace {
 
 constexpr int kTileM = 128;
-constexpr int kTileN = 128;
 constexpr int kTileK = 32;   // fp32 elements per 128-byte swizzle row
 constexpr int kStagesMax = 4;  // pipeline depth; 3 when MN-major operands also need raw buffers
 constexpr int kThreads = 192;  // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 epilogue
-constexpr int kTileBytes = kTileM * kTileK * 4;  // 16 KB per operand tile and stage
+constexpr int kTileBytes = kTileM * kTileK * 4;  // 16 KB: the A tile of a stage (B: BN / 128 of it)
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 
@@ -89,12 +89,10 @@ __device__ __forceinline__ uint64_t smem_desc(const void* p, unsigned lbo, unsig
 }
 
 // Instruction descriptor, kind::tf32: fp32 accumulate, tf32 A and B.
-__host__ __device__ constexpr uint32_t instr_desc(bool a_mn, bool b_mn) {
+__host__ __device__ constexpr uint32_t instr_desc(int bn) {
   return (1u << 4)                              // D format F32
-         | (2u << 7) | (2u << 10)               // A, B format TF32
-         | (static_cast<uint32_t>(a_mn) << 15)  // A major (1 = MN)
-         | (static_cast<uint32_t>(b_mn) << 16)  // B major
-         | (static_cast<uint32_t>(kTileN >> 3) << 17) | (static_cast<uint32_t>(kTileM >> 4) << 24);
+         | (2u << 7) | (2u << 10)               // A, B format TF32, both K-major
+         | (static_cast<uint32_t>(bn >> 3) << 17) | (static_cast<uint32_t>(kTileM >> 4) << 24);
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, bool accumulate) {
@@ -112,13 +110,13 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 // One operand tile (128 rows of the MMA's M or N x 32 of K) into stage memory.
 // K-major: one box {32 K, 128 rows} straight into the MMA layout. MN-major:
 // four boxes {32 MN, 32 K}, 4 KB apart, into the raw buffer for the transposer.
-template <bool kMN>
+template <bool kMN, int ROWS>
 __device__ __forceinline__ void load_tile(float* dst, const CUtensorMap* map, int mn0, int k0, uint64_t* bar) {
   if (!kMN) {
     tma_load_2d(dst, map, k0, mn0, bar);
   } else {
 #pragma unroll
-    for (int i = 0; i < kTileM / 32; ++i) tma_load_2d(dst + i * 32 * kTileK, map, mn0 + 32 * i, k0, bar);
+    for (int i = 0; i < ROWS / 32; ++i) tma_load_2d(dst + i * 32 * kTileK, map, mn0 + 32 * i, k0, bar);
   }
 }
 
@@ -134,14 +132,16 @@ __device__ __forceinline__ unsigned swz(unsigned row, unsigned col) {
 // and dpre^T, x in dW are MN-major in memory, so each stage is transposed here.
 // Reads: one swizzled 128-byte row per k across the lanes (conflict-free);
 // writes: one 16-byte chunk per lane (4 wavefronts per 512 bytes, the minimum).
+template <int ROWS>
 __device__ __forceinline__ void transpose_tile(const float* raw, float* kmaj, int t) {
   const char* rb = reinterpret_cast<const char*>(raw);
   char* kb = reinterpret_cast<char*>(kmaj);
   const int mn_lo = t & 31;  // lane within the 32-wide chunk
+  constexpr int kChunks = ROWS / 32;
 #pragma unroll
-  for (int it = 0; it < 8; ++it) {
-    const int chunk = it & 3;                     // MN chunk (32 rows of the MMA tile)
-    const int kq = (t >> 5) + 4 * (it >> 2);      // k quad 0..7
+  for (int it = 0; it < 2 * kChunks; ++it) {  // (ROWS x 8 quads) / 128 threads
+    const int chunk = it % kChunks;                          // MN chunk (32 rows of the MMA tile)
+    const int kq = (t >> 5) + 4 * (it / kChunks);            // k quad 0..7
     const int mn = chunk * 32 + mn_lo;
     float v[4];
 #pragma unroll
@@ -157,42 +157,40 @@ __device__ __forceinline__ uint64_t tile_desc(const float* tile, int j) {
 }
 
 struct GemmArgs {
-  int M, N;          // output extent (rows x cols of D)
+  int M, N;          // extent of D (M x N)
   int k_blocks;      // 32-wide K blocks per split
   int k_total;       // K extent (for the split range)
-  float* out;        // D, row-major with leading dimension ldo
+  float* out;        // row-major output with leading dimension ldo: D, or D^T when transposed
   long long ldo;
   int accumulate;    // 1: out += D (atomic, split-K safe); 0: out = D
+  int transposed;    // 1: out[n][m] = D[m][n]
 };
 
-constexpr int kRawBytes = kTileM * kTileK * 4;  // per MN-major operand and stage
-
-template <bool kAMN, bool kBMN>
-__host__ __device__ constexpr int gemm_stages() {
-  return (kAMN || kBMN) ? 3 : kStagesMax;
-}
-template <bool kAMN, bool kBMN>
+template <bool kAMN, bool kBMN, int BN, int STAGES>
 __host__ __device__ constexpr int gemm_smem() {
-  return gemm_stages<kAMN, kBMN>() * (2 * kTileBytes + (kAMN ? kRawBytes : 0) + (kBMN ? kRawBytes : 0)) +
-         4 * 32 * 33 * 4 + 256 + 1024;
+  return STAGES * ((kTileBytes + BN * kTileK * 4) * (1 + (kAMN || kBMN))) + 4 * 32 * 33 * 4 + 256 + 1024;
 }
 
 // D[M x N] (+)= A[M x K] . B[K x N]; blockIdx = (n tile, m tile, K split).
-template <bool kAMN, bool kBMN>
+// STAGES: pipeline depth (1 when K is a single block: several CTAs then share
+// an SM, so one CTA's epilogue stores overlap another's loads).
+template <bool kAMN, bool kBMN, int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     k_fc_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, GemmArgs g) {
   constexpr bool kTrans = kAMN || kBMN;
-  constexpr int kStages = gemm_stages<kAMN, kBMN>();
+  constexpr int kStages = STAGES;
+  constexpr int kBBytes = BN * kTileK * 4;
+  constexpr int kTmemCols = BN < 32 ? 32 : BN;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1 KB alignment for the 128B-swizzle atoms
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* a_tiles = reinterpret_cast<float*>(smem);
   float* b_tiles = reinterpret_cast<float*>(smem + kStages * kTileBytes);
-  unsigned char* p = smem + 2 * kStages * kTileBytes;
+  unsigned char* p = smem + kStages * (kTileBytes + kBBytes);
   float* a_raw = reinterpret_cast<float*>(p);
-  if (kAMN) p += kStages * kRawBytes;
+  if (kAMN) p += kStages * kTileBytes;
   float* b_raw = reinterpret_cast<float*>(p);
-  if (kBMN) p += kStages * kRawBytes;
+  if (kBMN) p += kStages * kBBytes;
   float* stage_out = reinterpret_cast<float*>(p);  // [4 warps][32][33]
   uint64_t* full = reinterpret_cast<uint64_t*>(p + 4 * 32 * 33 * 4);
   uint64_t* ready = full + kStages;   // transposed (MN-major operands only)
@@ -201,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * kTileN, m0 = blockIdx.y * kTileM;
+  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * kTileM;
   const int kb_begin = blockIdx.z * g.k_blocks;
   const int kb_end = min(kb_begin + g.k_blocks, (g.k_total + kTileK - 1) / kTileK);
   const int nkb = max(kb_end - kb_begin, 0);
@@ -217,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 1) {  // TMEM: 128 lanes x 128 fp32 columns of accumulator
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(kTileN));
+                 "n"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -230,20 +228,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < nkb; ++i) {
       const int s = i % kStages;
       if (i >= kStages) mbar_wait(empty + s, ((i / kStages) - 1) & 1);
-      mbar_expect_tx(full + s, 2 * kTileBytes);
+      mbar_expect_tx(full + s, kTileBytes + kBBytes);
       const int k0 = (kb_begin + i) * kTileK;
-      load_tile<kAMN>((kAMN ? a_raw : a_tiles) + s * kTileM * kTileK, &map_a, m0, k0, full + s);
-      load_tile<kBMN>((kBMN ? b_raw : b_tiles) + s * kTileN * kTileK, &map_b, n0, k0, full + s);
+      load_tile<kAMN, kTileM>((kAMN ? a_raw : a_tiles) + s * kTileM * kTileK, &map_a, m0, k0, full + s);
+      load_tile<kBMN, BN>((kBMN ? b_raw : b_tiles) + s * BN * kTileK, &map_b, n0, k0, full + s);
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer: one thread, tcgen05.mma kind::tf32 into TMEM ----
-    constexpr uint32_t idesc = instr_desc(false, false);
+    constexpr uint32_t idesc = instr_desc(BN);
     for (int i = 0; i < nkb; ++i) {
       const int s = i % kStages;
       mbar_wait((kTrans ? ready : full) + s, (i / kStages) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const float* at = a_tiles + s * kTileM * kTileK;
-      const float* bt = b_tiles + s * kTileN * kTileK;
+      const float* bt = b_tiles + s * BN * kTileK;
 #pragma unroll
       for (int j = 0; j < kTileK / 8; ++j) mma_tf32(tmem, tile_desc(at, j), tile_desc(bt, j), idesc, i > 0 || j > 0);
       mma_commit(empty + s);  // the stage is free once these MMAs have read it
@@ -256,8 +254,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = 0; i < nkb; ++i) {
         const int s = i % kStages;
         mbar_wait(full + s, (i / kStages) & 1);
-        if (kAMN) transpose_tile(a_raw + s * kTileM * kTileK, a_tiles + s * kTileM * kTileK, t);
-        if (kBMN) transpose_tile(b_raw + s * kTileN * kTileK, b_tiles + s * kTileN * kTileK, t);
+        if (kAMN) transpose_tile<kTileM>(a_raw + s * kTileM * kTileK, a_tiles + s * kTileM * kTileK, t);
+        if (kBMN) transpose_tile<BN>(b_raw + s * BN * kTileK, b_tiles + s * BN * kTileK, t);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> the MMA's async reads
         __syncwarp();
         if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(ready + s)) : "memory");
@@ -269,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(done, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       float* buf = stage_out + (warp - 2) * 32 * 33;
-      for (int c0 = 0; c0 < kTileN; c0 += 32) {
+      for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t v[32];
         const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c0);
         asm volatile(
@@ -282,6 +280,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         // lane = row (q * 32 + lane) of the tile: write its 32 columns, read back by column
+        if (g.transposed) {
+          // out[n][m]: for each n, the lanes (consecutive m) are consecutive words
+          const int row = m0 + q * 32 + lane;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int col = n0 + c0 + j;
+            if (row < g.M && col < g.N) {
+              float* o = g.out + static_cast<long long>(col) * g.ldo + row;
+              if (g.accumulate) atomicAdd(o, __uint_as_float(v[j]));
+              else *o = __uint_as_float(v[j]);
+            }
+          }
+          continue;
+        }
 #pragma unroll
         for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = __uint_as_float(v[j]);
         __syncwarp();
@@ -301,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTileN));
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
 }
 
 // Transposes the A x H weight into the K-major [H][pitch] operand of dx (zero pad).
@@ -365,19 +377,20 @@ bool make_map(CUtensorMap* m, const float* base, long long inner, long long oute
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <bool kAMN, bool kBMN>
+template <bool kAMN, bool kBMN, int BN, int STAGES>
 int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& g, int splits, cudaStream_t s) {
   static int configured[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  constexpr int smem = gemm_smem<kAMN, kBMN>();
+  constexpr int smem = gemm_smem<kAMN, kBMN, BN, STAGES>();
   if (dev >= 0 && dev < 64 && !configured[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(k_fc_gemm<kAMN, kBMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(k_fc_gemm<kAMN, kBMN, BN, STAGES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     configured[dev] = 1;
   }
-  const dim3 grid((g.N + kTileN - 1) / kTileN, (g.M + kTileM - 1) / kTileM, splits);
-  k_fc_gemm<kAMN, kBMN><<<grid, kThreads, smem, s>>>(ma, mb, g);
+  const dim3 grid((g.N + BN - 1) / BN, (g.M + kTileM - 1) / kTileM, splits);
+  k_fc_gemm<kAMN, kBMN, BN, STAGES><<<grid, kThreads, smem, s>>>(ma, mb, g);
   return cudaGetLastError();
 }
 
@@ -416,19 +429,32 @@ int fc_backward(const float* g, const float* x, const float* w, float* dw, float
     const int rpb = 256;
     k_bias_grad<<<dim3((A + 255) / 256, (rows + rpb - 1) / rpb), 256, 0, s>>>(gp, ldg, rows, A, rpb, db);
   }
-  // dW[A x H] += g^T x: A operand g^T (M = A contiguous -> MN-major), B operand x
-  // (N = H contiguous -> MN-major); K = rows, split so the grid fills the SMs.
+  // dW[A x H] += g^T x, K = rows (split so the grid fills the SMs). Small
+  // alphabets (A <= 32) run it as dW^T = x^T g: M = H, N = A = one 32-wide
+  // tile (no padding of A to 128), written transposed. Otherwise M = A, N = H.
+  // Both operands are MN-major in memory (transposed per stage in smem).
   if (dw) {
     CUtensorMap ma, mb;
-    if (!make_map(&ma, gp, A, rows, ldg, kTileK) || !make_map(&mb, x, H, rows, H, kTileK))
-      return cudaErrorInvalidValue;
-    GemmArgs ga{A, H, 0, rows, dw, H, 1};
-    const int tiles = ((A + kTileM - 1) / kTileM) * ((H + kTileN - 1) / kTileN);
     const int kb = (rows + kTileK - 1) / kTileK;
-    int splits = std::max(1, std::min(kb, (2 * sm_count + tiles - 1) / tiles));
-    ga.k_blocks = (kb + splits - 1) / splits;
-    splits = (kb + ga.k_blocks - 1) / ga.k_blocks;
-    const int e = launch_gemm<true, true>(ma, mb, ga, splits, s);
+    auto split_for = [&](int tiles) {
+      const int sp = std::max(1, std::min(kb, (4 * sm_count + tiles - 1) / tiles));
+      const int kpb = (kb + sp - 1) / sp;
+      return std::make_pair((kb + kpb - 1) / kpb, kpb);
+    };
+    int e;
+    if (A <= 32) {
+      if (!make_map(&ma, x, H, rows, H, kTileK) || !make_map(&mb, gp, A, rows, ldg, kTileK))
+        return cudaErrorInvalidValue;
+      const auto sp = split_for((H + kTileM - 1) / kTileM);
+      GemmArgs ga{H, A, sp.second, rows, dw, H, 1, 1};
+      e = launch_gemm<true, true, 32, 4>(ma, mb, ga, sp.first, s);
+    } else {
+      if (!make_map(&ma, gp, A, rows, ldg, kTileK) || !make_map(&mb, x, H, rows, H, kTileK))
+        return cudaErrorInvalidValue;
+      const auto sp = split_for(((A + kTileM - 1) / kTileM) * ((H + 127) / 128));
+      GemmArgs ga{A, H, sp.second, rows, dw, H, 1, 0};
+      e = launch_gemm<true, true, 128, 3>(ma, mb, ga, sp.first, s);
+    }
     if (e != cudaSuccess) return e;
   }
   // dx[rows x H] = g W: A operand g (K = A contiguous -> K-major), B operand
@@ -438,10 +464,11 @@ int fc_backward(const float* g, const float* x, const float* w, float* dw, float
     float* wt = reinterpret_cast<float*>(static_cast<unsigned char*>(workspace) + pad_bytes(rows, A));
     k_transpose_w<<<dim3((H + 31) / 32, (pitch + 31) / 32), dim3(32, 8), 0, s>>>(w, A, H, wt, pitch);
     CUtensorMap ma, mb;
-    if (!make_map(&ma, gp, A, rows, ldg, kTileM) || !make_map(&mb, wt, A, H, pitch, kTileN))
+    if (!make_map(&ma, gp, A, rows, ldg, kTileM) || !make_map(&mb, wt, A, H, pitch, 128))
       return cudaErrorInvalidValue;
-    GemmArgs gx{rows, H, (A + kTileK - 1) / kTileK, A, dx, H, 0};
-    const int e = launch_gemm<false, false>(ma, mb, gx, 1, s);
+    GemmArgs gx{rows, H, (A + kTileK - 1) / kTileK, A, dx, H, 0, 0};
+    const int e = A <= kTileK ? launch_gemm<false, false, 128, 1>(ma, mb, gx, 1, s)
+                              : launch_gemm<false, false, 128, 4>(ma, mb, gx, 1, s);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
