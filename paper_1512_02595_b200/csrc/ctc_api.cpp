@@ -50,10 +50,11 @@ class Staging {
   }
 
  private:
-  // Four calls' worth of blobs: a length-split call takes one slot per
-  // sub-batch (kDevSplitMax), so the host can still run several calls ahead
-  // of the GPU before acquire() waits on a slot's previous copy.
-  static constexpr int kSlots = 32;
+  // One slot per call (a length-split call packs its sub-batches' blobs into
+  // one slot), so the host can run 8 calls ahead of the GPU. Growing a slot
+  // is a cudaMallocHost, so the slots must be warm before any timed call:
+  // few of them, reused round-robin.
+  static constexpr int kSlots = 8;
   struct Slot {
     void* ptr = nullptr;
     size_t cap = 0;
@@ -76,7 +77,11 @@ struct Profiler {
   int slots = 0;
   int device = -1;
   long long calls = 0;
-  std::vector<cudaEvent_t> ev;  // 4 per slot
+  // 6 per slot: 0 start, 1 after k_pair, 2 after the dense pass, 3 end (all on
+  // the caller's stream); 4, 5 around k_dense_soft on the side stream when the
+  // dense pass overlaps k_pair (then the "dense" stage is that kernel alone)
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> side;  // per slot: 1 when events 4, 5 were recorded
   void reset() {
     for (auto e : ev)
       if (e) cudaEventDestroy(e);
@@ -86,16 +91,21 @@ struct Profiler {
   }
   bool ready(int dev) {
     if (slots <= 0) return false;
-    if (device != dev || static_cast<int>(ev.size()) != 4 * slots) {
+    if (device != dev || static_cast<int>(ev.size()) != 6 * slots) {
       reset();
-      ev.assign(4 * slots, nullptr);
+      ev.assign(6 * slots, nullptr);
+      side.assign(slots, 0);
       for (auto& e : ev)
         if (cudaEventCreate(&e) != cudaSuccess) return false;
       device = dev;
     }
     return calls < slots;
   }
-  void mark(int i, cudaStream_t s) { cudaEventRecord(ev[4 * calls + i], s); }
+  void mark(int i, cudaStream_t s) {
+    cudaEventRecord(ev[6 * calls + i], s);
+    if (i == 0) side[calls] = 0;
+    if (i == 4) side[calls] = 1;
+  }
   bool suspended = false;  // inside a length-split call: one record for the whole call
 };
 
@@ -292,9 +302,13 @@ bool dual_mode(int B) {
   return 2 * B > sm_count();
 }
 
+// `pinned_slice`: a pinned staging region for this call's metadata blob
+// (>= make_layout(...).meta_end bytes) provided by run_split, which owns the
+// slot and its reuse event; nullptr: take a slot of this thread's ring.
 ds2ctc_status run(const float* acts, float* grads, const int* flat_labels, const int* label_lengths,
                   const int* input_lengths, int A, int B, int blank, float* costs, void* workspace,
-                  size_t workspace_bytes, bool check_ws, void* stream, int ld = 0) {
+                  size_t workspace_bytes, bool check_ws, void* stream, int ld = 0,
+                  unsigned char* pinned_slice = nullptr) {
   ds2ctc_status st = validate(label_lengths, input_lengths, A, B, blank, flat_labels);
   if (st != DS2CTC_STATUS_SUCCESS) return st;
   if (B == 0) return DS2CTC_STATUS_SUCCESS;
@@ -312,12 +326,12 @@ ds2ctc_status run(const float* acts, float* grads, const int* flat_labels, const
   auto* ws = static_cast<unsigned char*>(workspace);
   auto s = static_cast<cudaStream_t>(stream);
   cudaEvent_t ev = nullptr;
-  void* pinned = staging_for_current_device().acquire(meta_used, &ev);
+  void* pinned = pinned_slice != nullptr ? pinned_slice : staging_for_current_device().acquire(meta_used, &ev);
   if (pinned == nullptr) return DS2CTC_STATUS_MEMOPS_FAILED;
   std::memcpy(pinned, blob.data(), meta_used);
   if (cudaMemcpyAsync(ws, pinned, meta_used, cudaMemcpyHostToDevice, s) != cudaSuccess)
     return DS2CTC_STATUS_MEMOPS_FAILED;
-  if (cudaEventRecord(ev, s) != cudaSuccess) return DS2CTC_STATUS_MEMOPS_FAILED;
+  if (ev != nullptr && cudaEventRecord(ev, s) != cudaSuccess) return DS2CTC_STATUS_MEMOPS_FAILED;
 
   const bool fused = A <= kFusedMaxAlphabet;
   PairArgs a{};
@@ -375,7 +389,9 @@ ds2ctc_status run(const float* acts, float* grads, const int* flat_labels, const
   if (launch_pair(a, stream) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
   if (timed) prof.mark(1, s);
   if (ov != nullptr) {
+    if (timed) prof.mark(4, ov->side);
     const bool ok = launch_dense_soft(a, grads != nullptr, ov->side) == cudaSuccess;
+    if (timed) prof.mark(5, ov->side);
     // the caller's stream waits for the side stream on every path (ordering)
     if (cudaEventRecord(ov->join, ov->side) != cudaSuccess || cudaStreamWaitEvent(s, ov->join, 0) != cudaSuccess ||
         !ok)
@@ -692,6 +708,15 @@ ds2ctc_status run_split(const float* acts, float* grads, const int* flat_labels,
     return result;
   };
   if (forked < p.n) return join(DS2CTC_STATUS_EXECUTION_FAILED);
+  // one staging slot for the whole call: the sub-batches' metadata blobs side by side
+  size_t blob_off[kDevSplitMax + 1];
+  blob_off[0] = 0;
+  for (int c = 0; c < p.n; ++c)
+    blob_off[c + 1] = blob_off[c] + (make_layout(label_lengths + p.b0[c], input_lengths + p.b0[c], A,
+                                                 p.b0[c + 1] - p.b0[c]).meta_end + 255) / 256 * 256;
+  cudaEvent_t slot_ev = nullptr;
+  auto* pinned = static_cast<unsigned char*>(staging_for_current_device().acquire(blob_off[p.n], &slot_ev));
+  if (pinned == nullptr) return join(DS2CTC_STATUS_MEMOPS_FAILED);
   int t_max = 0;
   for (int b = 0; b < B; ++b) t_max = std::max(t_max, input_lengths[b]);
   for (int c = 0; c < p.n; ++c) {
@@ -709,10 +734,15 @@ ds2ctc_status run_split(const float* acts, float* grads, const int* flat_labels,
     st = run(acts + col, grads ? grads + col : nullptr, flat_labels + p.lab0[c], label_lengths + p.b0[c],
              input_lengths + p.b0[c], A, p.b0[c + 1] - p.b0[c], blank, costs + p.b0[c],
              static_cast<unsigned char*>(workspace) + p.ws_off[c], p.ws_off[c + 1] - p.ws_off[c], true,
-             c == 0 ? stream : ss.s[c - 1], B);
-    if (st != DS2CTC_STATUS_SUCCESS) return join(st);
+             c == 0 ? stream : ss.s[c - 1], B, pinned + blob_off[c]);
+    if (st != DS2CTC_STATUS_SUCCESS) {
+      st = join(st);
+      cudaEventRecord(slot_ev, s0);  // the slot is reusable once s0 passes every sub-batch's copy
+      return st;
+    }
   }
   st = join(DS2CTC_STATUS_SUCCESS);
+  if (cudaEventRecord(slot_ev, s0) != cudaSuccess && st == DS2CTC_STATUS_SUCCESS) st = DS2CTC_STATUS_EXECUTION_FAILED;
   if (st != DS2CTC_STATUS_SUCCESS) return st;
   if (timed) {
     prof.mark(1, s0);
@@ -888,10 +918,11 @@ ds2ctc_status ds2ctc_profile_enable(int slots) {
 ds2ctc_status ds2ctc_profile_read(int call_index, float* ms) {
   Profiler& p = profiler();
   if (ms == nullptr || call_index < 0 || call_index >= p.calls) return DS2CTC_STATUS_INVALID_VALUE;
-  cudaEvent_t* e = p.ev.data() + 4 * call_index;
+  cudaEvent_t* e = p.ev.data() + 6 * call_index;
   if (cudaEventSynchronize(e[3]) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  const bool side = p.side[call_index] != 0;
   if (cudaEventElapsedTime(&ms[0], e[0], e[1]) != cudaSuccess ||
-      cudaEventElapsedTime(&ms[1], e[1], e[2]) != cudaSuccess ||
+      cudaEventElapsedTime(&ms[1], side ? e[4] : e[1], side ? e[5] : e[2]) != cudaSuccess ||
       cudaEventElapsedTime(&ms[2], e[2], e[3]) != cudaSuccess ||
       cudaEventElapsedTime(&ms[3], e[0], e[3]) != cudaSuccess)
     return DS2CTC_STATUS_EXECUTION_FAILED;

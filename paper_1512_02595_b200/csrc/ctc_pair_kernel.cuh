@@ -288,6 +288,12 @@ struct Epoch {
 // K <= 6 keeps at most three chain warps (5 warps per CTA: pick_K takes the
 // smallest K with L + 1 <= 3 * 28 * K); only K = 8 (labels longer than 671)
 // may use up to ten.
+// Phase-2 epochs whose last column is sampled for the per-frame
+// renormalisation: every DS2CTC_NORM_EVERY-th epoch (1 = all).
+#ifndef DS2CTC_NORM_EVERY
+#define DS2CTC_NORM_EVERY 1
+#endif
+
 template <int K>
 constexpr int max_threads_for() {
   return K == 1 ? 32 * 8 : K <= 6 ? 32 * 5 : kMaxThreads;
@@ -345,6 +351,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   float* occs = reinterpret_cast<float*>(smem + g.off_occ);
   float* nrm = reinterpret_cast<float*>(smem + g.off_nrm);  // [2][NPW] frame mass per chain thread
   const int NPW = column_threads(g.max_L, K);
+  float inv_keep = 1.f;  // gradient warp: the frame-mass factor of the last sampled epoch
   const int CT = column_threads(L, K);
   unsigned long long* ring = reinterpret_cast<unsigned long long*>(smem + g.off_ring);
   int* s_lab = reinterpret_cast<int*>(smem + g.off_meta);
@@ -352,8 +359,8 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   int* s_kstart = s_kchar + u.nkey;
   int* s_kpos = s_kstart + u.nkey + 1;
   int* s_slotpos = s_kpos + L;  // slot of each label position
-  int* s_kq = s_slotpos + L + 1;  // slot-sorted positions packed as pos | slot << 16
-  short* s_slot = reinterpret_cast<short*>(s_kq + L + 1);  // fused: symbol -> slot
+  int* s_rank = s_slotpos + L + 1;  // slot-sorted rank of each label position (its occupancy-row word)
+  short* s_slot = reinterpret_cast<short*>(s_rank + L + 1);  // fused: symbol -> slot
   double* red = reinterpret_cast<double*>(smem + g.off_red);
   // poisoned frames (a NaN or +inf logit, or, with the whole row staged, every
   // logit -inf): log_softmax_rows (ctc.cpp:24-37) makes the whole row NaN in
@@ -566,7 +573,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     for (int j = t2; j < u.nkey; j += n2)
       for (int q = s_kstart[j]; q < s_kstart[j + 1]; ++q) {
         s_slotpos[s_kpos[q]] = j;
-        s_kq[q] = occ_word(s_kpos[q], K, dir) | (j << 16);  // the position's occupancy-row word
+        s_rank[s_kpos[q]] = q;
       }
   }
   __syncthreads();
@@ -581,12 +588,13 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
   // Label sums of slots [jlo, jhi) of the epoch's frames; returns this lane's
   // (frame's) unnormalised total over them. The full call (all slots) also
   // writes the blank slot; the drain splits the slots over several warps.
-  auto grad_occ_part = [&](const Epoch& e, int half, int jlo, int jhi, float& inv_out) -> float {
+  auto grad_occ_part = [&](const Epoch& e, int half, int jlo, int jhi, float& inv_out, bool sampled,
+                           int fr) -> float {  // fr: this lane's frame within the epoch
     if (e.phase != 2) return 0.f;
     const int n = e.k1 - e.k0;
-    const int k = e.k0 + (lane < n ? lane : 0);
+    const int k = e.k0 + (fr < n ? fr : 0);
     const float* elr = el + (k & M2) * g.estride;
-    float* oc = occs + (half * 32 + lane) * g.ostride;
+    float* oc = occs + (half * 32 + fr) * g.ostride;
     // Label cells in one flat pass over the slot-sorted positions of slots
     // >= 1 (every one of them has positions), flushing at slot changes. The
     // blank slot is the rest of the frame's unit mass: sum_s gamma(s, t) = 1
@@ -603,35 +611,48 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
 #ifdef DS2CTC_EXP_NONORM
     const float inv = 1.f;
 #else
-    float z = 0.f;
-    for (int j = lane; j < CT; j += 32) z += nrm[half * NPW + j];
+    // epoch e was sampled (its frame mass written into nrm[half]) iff the chain
+    // ran it as an epoch counter that is a multiple of DS2CTC_NORM_EVERY;
+    // otherwise the last sampled epoch's factor stays in force
+    if (sampled) {
+      float z = 0.f;
+      for (int j = lane; j < CT; j += 32) z += nrm[half * NPW + j];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
-    const float inv = z > 0.5f && z < 2.f ? __frcp_rn(z) : 1.f;  // a sane mass, else leave as is
+      for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+      inv_keep = z > 0.5f && z < 2.f ? __frcp_rn(z) : 1.f;  // a sane mass, else leave as is
+    }
+    const float inv = inv_keep;
 #endif
     inv_out = inv;
+    // The occupancy row is in slot-sorted order (the chain lanes store each
+    // label cell at its position's slot-sorted rank), so the slots are
+    // contiguous runs: plain loads (no index load in front of each), and
+    // the run boundaries are warp-uniform.
     float acc = 0.f, tot = 0.f;
     int cur = jlo;
     int q = s_kstart[jlo];
     const int qend = s_kstart[jhi];
+    int nb = s_kstart[jlo + 1];  // end of the current slot's run
+    auto flush = [&]() {
+      oc[cur] = acc * inv;
+      tot += acc;
+      acc = 0.f;
+      nb = s_kstart[++cur + 1];
+    };
     for (; q + 3 < qend; q += 4) {
-      const int w0 = s_kq[q], w1 = s_kq[q + 1], w2 = s_kq[q + 2], w3 = s_kq[q + 3];
-      const float v0 = elr[w0 & 0xFFFF], v1 = elr[w1 & 0xFFFF], v2 = elr[w2 & 0xFFFF], v3 = elr[w3 & 0xFFFF];
-      const int j0 = w0 >> 16, j1 = w1 >> 16, j2 = w2 >> 16, j3 = w3 >> 16;
-      if (j0 != cur) { oc[cur] = acc * inv; tot += acc; acc = 0.f; cur = j0; }
+      const float v0 = elr[q], v1 = elr[q + 1], v2 = elr[q + 2], v3 = elr[q + 3];
+      if (q == nb) flush();
       acc += v0;
-      if (j1 != cur) { oc[cur] = acc * inv; tot += acc; acc = 0.f; cur = j1; }
+      if (q + 1 == nb) flush();
       acc += v1;
-      if (j2 != cur) { oc[cur] = acc * inv; tot += acc; acc = 0.f; cur = j2; }
+      if (q + 2 == nb) flush();
       acc += v2;
-      if (j3 != cur) { oc[cur] = acc * inv; tot += acc; acc = 0.f; cur = j3; }
+      if (q + 3 == nb) flush();
       acc += v3;
     }
     for (; q < qend; ++q) {
-      const int w0 = s_kq[q];
-      const int j0 = w0 >> 16;
-      if (j0 != cur) { oc[cur] = acc * inv; tot += acc; acc = 0.f; cur = j0; }
-      acc += elr[w0 & 0xFFFF];
+      if (q == nb) flush();
+      acc += elr[q];
     }
     if (jhi > jlo) {
       oc[cur] = acc * inv;
@@ -639,10 +660,22 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     }
     return tot;
   };
+  // Epochs of <= 16 frames (P = 16 at long labels): the two half-warps take
+  // the same frames and half of the key slots each, so the pass costs half
+  // the label positions per lane instead of idling 16 lanes.
   auto grad_occ = [&](const Epoch& e, int half) {
     if (e.phase != 2) return;
     float inv = 1.f;
-    const float tot = grad_occ_part(e, half, 1, u.nkey, inv);
+    const bool sampled = ((ep - 1) % DS2CTC_NORM_EVERY) == 0;
+    if (e.k1 - e.k0 <= 16) {
+      const int hl = lane >> 4, fr = lane & 15;
+      const int mid = 1 + (u.nkey - 1) / 2;
+      float tot = grad_occ_part(e, half, hl ? mid : 1, hl ? u.nkey : mid, inv, sampled, fr);
+      tot += __shfl_xor_sync(0xffffffffu, tot, 16);
+      if (hl == 0) occs[(half * 32 + fr) * g.ostride] = 1.f - tot * inv;  // the blank slot
+      return;
+    }
+    const float tot = grad_occ_part(e, half, 1, u.nkey, inv, sampled, lane);
     occs[(half * 32 + lane) * g.ostride] = 1.f - tot * inv;  // the blank slot
   };
   auto grad_write = [&](const Epoch& e, int half) {
@@ -914,8 +947,11 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     const int sl = 2 * K * (has_l[p] ? ctid : ctid0) + 2 * p + (dir == 0 ? 2 : -1);
     pslot[p] = column_slot_word(max(sl, 0), K, pdir);
   }
-  // occupancy-row word of each label cell: this lane's own block slot
-  const int el_base = cwarp * K * 32 + lane;
+  // occupancy-row word of each label cell: its position's slot-sorted rank
+  // (cells without a label: the row's spare word L)
+  int el_idx[K];
+#pragma unroll
+  for (int p = 0; p < K; ++p) el_idx[p] = has_l[p] ? s_rank[dir == 0 ? ctid * K + p : ctid * K + p - 1] : L;
   // writer threads of the first / last slot
   const int oct = owner ? ctid : ctid0;
   const int poff_lo = column_word(max(dir == 0 ? oct : oct - 1, 0), 2 * K, K, pdir);
@@ -955,7 +991,7 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
       const float ol = (dir == 0 ? p == K - 1 : p != 0) ? o_hi : o_lo;
       // linear occupancy 2^gamma; unconditional: cells without a label write their own unused word
       const float ml = ex2(ol + (rl + d[p]));
-      elr[el_base + p * 32] = ml;
+      elr[el_idx[p]] = ml;
 #ifndef DS2CTC_EXP_NOFRAMEMASS
       if constexpr (full) {
         // blank 2i: forward partner slot 2i + 1, backward partner slot 2i (both thread ctid)
@@ -1002,6 +1038,9 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     for (int k = e.k0 + 1; k < e.k1;) {
       const int kb = min(e.k1, k + (RS - since));
       since += kb - k;
+      // (Shuffling the neighbour before the re-centring -- the value in the
+      // pre-step offset -- measured slower: 151.7 vs 145.0 us per English
+      // k_pair, gpurun_out/r02ab2; the scheduler already overlaps them.)
       if (ph2) {
         for (; k < kb; ++k) {
           STEP_STAMP(k, e, 0);
@@ -1027,7 +1066,8 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
       }
     }
     if (ph2) {
-      occupancy_column(e.k1 - 1, e, std::true_type{});
+      if (ep % DS2CTC_NORM_EVERY == 0) occupancy_column(e.k1 - 1, e, std::true_type{});
+      else occupancy_column(e.k1 - 1, e, std::false_type{});
     } else {
       store_column(e.k1 - 1, e);
       fence_async_shared();  // the service warp bulk-stores this epoch's columns
@@ -1221,7 +1261,8 @@ __device__ __forceinline__ void pair_body(const PairArgs& a, unsigned char* smem
     if (grad_warp || (warp >= 1 && warp <= NCW)) {
       const int ns = u.nkey - 1;
       float inv = 1.f;
-      const float t = grad_occ_part(prev, (ep - 1) & 1, 1 + ns * part / nparts, 1 + ns * (part + 1) / nparts, inv);
+      const float t = grad_occ_part(prev, (ep - 1) & 1, 1 + ns * part / nparts, 1 + ns * (part + 1) / nparts, inv,
+                                    ((ep - 1) % DS2CTC_NORM_EVERY) == 0, lane);
       red_f[part * 32 + lane] = t;
       if (grad_warp) red_f[nparts * 32 + lane] = inv;
     }

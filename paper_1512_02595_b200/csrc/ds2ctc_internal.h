@@ -118,16 +118,9 @@ DS2CTC_HD inline int column_word(int j, int q, int K, int dir) {
   return (j / kOwnedLanes) * column_block(K) + q * 32 + thread_lane(j, dir);
 }
 DS2CTC_HD inline int column_slot_word(int slot, int K, int dir) { return column_word(slot / (2 * K), slot % (2 * K), K, dir); }
-// Occupancy rows (phase 2), warp-blocked the same way: lane l of chain warp w
-// writes its p-th label cell at w * K * 32 + p * 32 + l. Label position li
-// belongs to chain thread li / K, pair li % K (forward) or (li + 1) / K,
-// (li + 1) % K (backward: pair p of thread j holds label cell 2(jK + p) - 1).
-DS2CTC_HD inline int occ_row_words(int L, int K) { return chain_warps_for(L, K) * K * 32; }
-DS2CTC_HD inline int occ_word(int li, int K, int dir) {
-  const int x = dir == 0 ? li : li + 1;
-  const int j = x / K, p = x % K;
-  return (j / kOwnedLanes) * K * 32 + p * 32 + thread_lane(j, dir);
-}
+// Occupancy rows (phase 2): each label cell's occupancy at its position's
+// slot-sorted rank (word L is the spare of cells without a label), so the
+// gradient warp sums each key slot as one contiguous run.
 
 // max_L_all: the longest label of the whole batch (it fixes K and hence the
 // stored column layout, see make_layout); max_L: the longest that runs.
@@ -143,7 +136,7 @@ inline Geometry make_geometry(int max_L_all, int max_L, int max_nkey, int A, boo
   for (int P = 32; P >= 2; P /= 2) {
     g.P = P;
     g.xstride = g.SW | 1;
-    g.estride = occ_row_words(max_L, g.K) | 1;
+    g.estride = (max_L + 1) | 1;  // slot-sorted label positions + a spare word
     g.ostride = max_nkey | 1;
     int off = 0;
     auto take = [&](int bytes) {

@@ -342,6 +342,29 @@ __global__ void k_bias_grad(const float* __restrict__ g, long long ldg, int rows
   }
 }
 
+// Small alphabets (A <= 32): one pass over the gradient rows that both
+// re-pitches them to the TMA-legal 32 floats (zero fill; dst may be null when
+// A % 4 == 0) and sums db. 256 threads = 8 rows x 32 columns per iteration,
+// per-thread column sums, then the 8 row groups folded in shared memory.
+__global__ void __launch_bounds__(256) k_pad_bias(const float* __restrict__ src, int A, long long rows,
+                                                  float* __restrict__ dst, int pitch, float* __restrict__ db) {
+  __shared__ float part[8][33];
+  const int c = threadIdx.x & 31, rg = threadIdx.x >> 5;
+  float acc = 0.f;
+  for (long long r = blockIdx.x * 8LL + rg; r < rows; r += gridDim.x * 8LL) {
+    const float v = c < A ? src[r * A + c] : 0.f;
+    acc += v;
+    if (dst != nullptr && c < pitch) dst[r * pitch + c] = v;
+  }
+  part[rg][c] = acc;
+  __syncthreads();
+  if (rg == 0 && db != nullptr && c < A) {
+    float s = 0.f;
+    for (int i = 0; i < 8; ++i) s += part[i][c];
+    atomicAdd(db + c, s);
+  }
+}
+
 // Pads rows of width A to the TMA-legal pitch (multiple of 4 floats), zero fill.
 __global__ void k_pad_rows(const float* __restrict__ src, int A, float* __restrict__ dst, int pitch, long long n) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
@@ -417,7 +440,16 @@ int fc_backward(const float* g, const float* x, const float* w, float* dw, float
   // The workspace always holds W^T for dx after the padded rows.
   const float* gp = g;
   long long ldg = A;
-  if (A % 4 != 0) {
+  if (A <= 32) {  // fused re-pitch + bias sum (one pass over the gradient)
+    const int pitch = (A + 3) / 4 * 4;
+    float* dst = A % 4 != 0 ? static_cast<float*>(workspace) : nullptr;
+    const long long blocks = std::min<long long>((rows + 7) / 8, 4LL * sm_count);
+    k_pad_bias<<<static_cast<unsigned>(blocks), 256, 0, s>>>(g, A, rows, dst, pitch, db);
+    if (dst) {
+      gp = dst;
+      ldg = pitch;
+    }
+  } else if (A % 4 != 0) {
     const int pitch = (A + 3) / 4 * 4;
     const long long n = static_cast<long long>(rows) * pitch;
     k_pad_rows<<<static_cast<unsigned>(std::min<long long>((n + 255) / 256, 4LL * sm_count * 8)), 256, 0, s>>>(
@@ -425,7 +457,7 @@ int fc_backward(const float* g, const float* x, const float* w, float* dw, float
     gp = static_cast<const float*>(workspace);
     ldg = pitch;
   }
-  if (db) {
+  if (db && A > 32) {
     const int rpb = 256;
     k_bias_grad<<<dim3((A + 255) / 256, (rows + rpb - 1) / rpb), 256, 0, s>>>(gp, ldg, rows, A, rpb, db);
   }

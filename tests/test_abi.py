@@ -132,3 +132,29 @@ def test_alignment_and_lattice_entry_points_validate_without_gpu():
                                   5, 1, 1, 1, 256, 1 << 20, None) == 1
     # an empty minibatch is a valid no-op (empty data-parallel shard)
     assert lib.ds2ctc_viterbi_align(None, None, None, None, 6, 0, 5, None, None, None, 0, None) == 0
+
+
+def test_fc_backward_entry_points_validate_without_gpu():
+    # the output-FC backward (nn.cpp:874-899) validates before touching the device
+    import ctypes
+
+    from paper_1512_02595_b200 import _lib
+
+    L = _lib.lib()
+    out = ctypes.c_size_t()
+    # A % 4 != 0: the gradient rows are re-pitched (rows x 32 floats) + W^T (H x 32)
+    assert L.ds2ctc_fc_backward_workspace_size(1000, 29, 256, ctypes.byref(out)) == 0
+    assert out.value >= 4 * (1000 * 32 + 256 * 32)
+    assert L.ds2ctc_fc_backward_workspace_size(1000, 6000, 256, ctypes.byref(out)) == 0
+    assert out.value == 4 * 256 * 6000  # aligned gradient rows: W^T only
+    assert L.ds2ctc_fc_backward_workspace_size(-1, 29, 256, ctypes.byref(out)) == 1
+    p = ctypes.c_void_p(256)  # never dereferenced: every case below fails validation or is a no-op
+    # rows == 0 is a no-op (an empty shard)
+    assert L.ds2ctc_fc_backward(p, p, p, p, p, p, 0, 29, 256, None, 0, None) == 0
+    # in_dim % 4 != 0 cannot be tiled by TMA: unsupported
+    assert L.ds2ctc_fc_backward(p, p, p, p, p, p, 10, 29, 250, None, 0, None) == 4
+    # misaligned buffers and a short workspace are invalid values
+    assert L.ds2ctc_fc_backward(ctypes.c_void_p(258), p, p, p, p, p, 10, 29, 256, None, 0, None) == 1
+    assert L.ds2ctc_fc_backward(p, p, p, p, p, p, 10, 29, 256, p, 16, None) == 1
+    # a NULL gradient with any requested output
+    assert L.ds2ctc_fc_backward(None, p, p, p, p, p, 10, 29, 256, p, 1 << 20, None) == 1
