@@ -114,7 +114,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB
     for src in CPP_SOURCES:
         obj = os.path.join(BUILD_, src + ".o")
         cmd = [os.environ.get("CXX", "g++"), "-O3", "-std=c++17", "-fPIC", "-Wall", "-Wextra", f"-I{INCLUDE}",
-               f"-I{CSRC}", f"-I{cuda_inc}", "-c", os.path.join(CSRC, src), "-o", obj]
+               f"-I{CSRC}", f"-I{cuda_inc}", *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
         subprocess.run(cmd, check=True)
         objs.append(obj)
     tmp = LIB_ + ".tmp"
