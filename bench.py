@@ -357,9 +357,11 @@ def main():
         if not torch.allclose(pair, ref_pair, rtol=1e-12, atol=0):
             raise RuntimeError(f"peer all-reduce {pair.tolist()} != NCCL {ref_pair.tolist()}")
 
+    dense_overlap = os.environ.get("DS2CTC_DENSE_OVERLAP", "1") != "0"  # the library's default (ctc_api.cpp)
     # kernels of ours per step: k_pair (+ k_dense + k_finalize for large A) + k_loss_sum / k_loss_allreduce
     if B:
-        launches_per_step = 1 + (2 if A > 128 else 0) + 1 + (5 if H else 0)  # fc: pad, bias, W^T, 2 GEMMs
+        # large A: k_dense + k_finalize, or (overlapped) k_dense_soft + k_dense_patch + k_finalize
+        launches_per_step = 1 + ((3 if dense_overlap else 2) if A > 128 else 0) + 1 + (5 if H else 0)  # fc: pad, bias, W^T, 2 GEMMs
     else:
         launches_per_step = 1
 
@@ -396,11 +398,27 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    # Soak: the same NUMBER of steps on every rank (a per-rank wall-clock loop
+    # can end one step apart, which leaves the peer mailboxes' sequence
+    # numbers one step out of phase: the last step of the rank ahead then
+    # waits for a peer step that never comes). Rank-local estimate, max over ranks.
     t_soak = time.perf_counter()
-    while time.perf_counter() - t_soak < args.soak_seconds:
+    for _ in range(3):
         flush.zero_()
         step()
-        torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    per_step = max((time.perf_counter() - t_soak) / 3, 1e-6)
+    n_soak = torch.tensor([int(args.soak_seconds / per_step)], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(n_soak, op=dist.ReduceOp.MAX)
+    for _ in range(int(n_soak.item())):
+        flush.zero_()
+        step()
+        if _ % 16 == 15:
+            torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    if peer is not None:
+        peer.check()  # a timed-out peer wait is an error, never a number
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -413,6 +431,8 @@ def main():
         step()
         ends[k].record(stream)
     torch.cuda.synchronize()
+    if peer is not None:
+        peer.check()
     if world > 1:
         dist.barrier()
     clocks = sampler.stop() if sampler else None
@@ -466,7 +486,7 @@ def main():
         # kernel: k_pair for small alphabets (it reads the logits and writes the gradient),
         # k_dense for large ones (the HBM pass).
         alg_bytes = 8.0 * float((il.astype(np.float64) * A).sum()) + 4.0 * float(ll.sum()) + 8.0 * B
-        dense_name = "k_dense_soft" if os.environ.get("DS2CTC_DENSE_OVERLAP", "1") != "0" else "k_dense"
+        dense_name = "k_dense_soft (k_dense_t<V, true>)" if dense_overlap else "k_dense (k_dense_t<V, false>)"
         dom_name, dom_ms = ("k_pair", pair_ms) if A <= 128 else (dense_name, dense_ms)
         achieved = alg_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
         # DRAM bytes per launch of the dominant kernel from one `ncu --set full`
@@ -523,7 +543,9 @@ def main():
             "scalar_reduce": ("nvlink peer mailboxes (ds2ctc_loss_sum_allreduce)" if peer is not None
                               else ("nccl all_reduce" if world > 1 else "none")),
             "frames_per_s": total_frames / (ms / 1e3),
-            "stage_ms": {"k_pair": pair_ms, ("k_dense_soft (concurrent with k_pair)" if A > 128 else "k_dense"): dense_ms,
+            "stage_ms": {"k_pair": pair_ms,
+                         ((("k_dense_soft (concurrent with k_pair)" if dense_overlap else "k_dense") if A > 128
+                           else "dense pass (none: fused into k_pair)")): dense_ms,
                          "k_finalize": final_ms},
             "roofline": {"bound": "hbm", "kernel": dom_name, "kernel_ms": dom_ms, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,

@@ -263,6 +263,36 @@ bool dense_overlap_enabled() {
   return on;
 }
 
+// Dynamic shared memory (unused) for k_dense_soft such that none of its
+// blocks fits on an SM next to the resident k_pair CTA(s): the concurrent
+// softmax pass then runs on the SMs k_pair leaves free and on each SM as soon
+// as k_pair releases it, instead of sharing issue slots with the chains
+// (co-resident, English-style chains slowed from 112 to 156 us at the
+// Mandarin shape). 0 = no exclusion: k_pair already fills the SM, or the
+// request would leave fewer than two dense blocks per SM on their own.
+// Opt-in (DS2CTC_DENSE_EXCLUDE=1): measured slower, 370 vs 345 us per
+// Mandarin step -- the 20 SMs k_pair leaves free move too little of the pass
+// and the request caps the later full-GPU part at 4 blocks per SM
+// (gpurun_out/r02mand).
+int dense_exclusion_smem(const Geometry& g) {
+  static const bool on = [] {
+    const char* v = std::getenv("DS2CTC_DENSE_EXCLUDE");
+    return v != nullptr && std::atoi(v) != 0;
+  }();
+  if (!on) return 0;
+  int dev = 0, cap = 0, reserved = 0, optin = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&cap, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+    return 0;
+  const int resident = g.dual ? 2 : 1;  // k_pair CTAs per SM
+  const int left = cap - resident * (g.smem + reserved);
+  const int x = ((left - reserved) / 16 + 1) * 16;  // x + reserved > left
+  if (x <= 0 || x > optin || 2 * (x + reserved) > cap) return 0;
+  return x;
+}
+
 struct OverlapStreams {
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
@@ -290,21 +320,37 @@ int sm_count() {
   return n[dev];
 }
 
-// DS2CTC_DUAL: 0 = never two clusters per SM pair, 1 = whenever it fits,
-// default: when the batch needs more than one wave (2B > SMs).
-bool dual_mode(int B) {
+// DS2CTC_DUAL: 0 = never two clusters per SM pair, 1 = whenever it fits.
+// Default: a makespan estimate. A k_pair CTA runs ~T_b dependent steps, so
+// one cluster per SM pair finishes the batch in about max(T_max, sum T / P)
+// step times (P = SMs / 2 cluster slots, LPT order); two per SM pair double
+// the slots but each chain shares its SMSPs and runs ~1.9x slower per step
+// (edge1500, K = 4: 1468 vs 765 cycles per step, profiles/r02_dual.txt).
+// Dual wins on uniform multi-wave batches (edge1500: 7.85 vs 8.17 ms) and
+// loses when one long utterance bounds the batch anyway (SortaGrad, 128
+// utterances per GPU: T_max 1500 vs sum T / 74 ~ 1340 -> 0.91 ms dual).
+constexpr double kDualSlowdown = 1.9;
+bool dual_mode(int B, const int* input_lengths) {
   static const int env = [] {
     const char* v = std::getenv("DS2CTC_DUAL");
     return v ? std::atoi(v) : -1;
   }();
   if (env == 0) return false;
   if (env > 0) return true;
-  return 2 * B > sm_count();
+  const int sms = sm_count();
+  if (2 * B <= sms) return false;  // one wave: nothing to gain
+  double sum = 0.0;
+  int tmax = 0;
+  for (int b = 0; b < B; ++b) {
+    sum += input_lengths[b];
+    tmax = std::max(tmax, input_lengths[b]);
+  }
+  const double slots = sms / 2;
+  const double single = std::max(static_cast<double>(tmax), sum / slots);
+  const double dual = kDualSlowdown * std::max(static_cast<double>(tmax), sum / (2.0 * slots));
+  return dual < single;
 }
 
-// `pinned_slice`: a pinned staging region for this call's metadata blob
-// (>= make_layout(...).meta_end bytes) provided by run_split, which owns the
-// slot and its reuse event; nullptr: take a slot of this thread's ring.
 ds2ctc_status run(const float* acts, float* grads, const int* flat_labels, const int* label_lengths,
                   const int* input_lengths, int A, int B, int blank, float* costs, void* workspace,
                   size_t workspace_bytes, bool check_ws, void* stream, int ld = 0,
@@ -363,7 +409,7 @@ ds2ctc_status run(const float* acts, float* grads, const int* flat_labels, const
   // pair when the geometry fits half the shared memory with epochs of >= 8
   // steps and <= 3 chain warps (K <= 4) -- the chains are latency-bound, so a
   // second resident utterance uses issue slots the first leaves idle.
-  if (dual_mode(B) && a.g.K <= 4 && a.g.nchain <= 3) {
+  if (dual_mode(B, input_lengths) && a.g.K <= 4 && a.g.nchain <= 3) {
     const Geometry g2 = make_geometry(max_L_all, mx.first, mx.second, A, fused, kSmemBudgetDual);
     if (static_cast<size_t>(g2.smem) <= kSmemBudgetDual && g2.P >= 8) {
       a.g = g2;
@@ -390,7 +436,7 @@ ds2ctc_status run(const float* acts, float* grads, const int* flat_labels, const
   if (timed) prof.mark(1, s);
   if (ov != nullptr) {
     if (timed) prof.mark(4, ov->side);
-    const bool ok = launch_dense_soft(a, grads != nullptr, ov->side) == cudaSuccess;
+    const bool ok = launch_dense_soft(a, grads != nullptr, dense_exclusion_smem(a.g), ov->side) == cudaSuccess;
     if (timed) prof.mark(5, ov->side);
     // the caller's stream waits for the side stream on every path (ordering)
     if (cudaEventRecord(ov->join, ov->side) != cudaSuccess || cudaStreamWaitEvent(s, ov->join, 0) != cudaSuccess ||

@@ -17,8 +17,10 @@ namespace ds2ctc {
 namespace {
 
 constexpr double kLn2 = 0.69314718055994530942;
-constexpr int kDenseThreads = 256;
-constexpr int kDenseVec = 8;  // float4 per thread in registers -> A <= 8192 on the vector path
+#ifndef DS2CTC_DENSE_THREADS
+#define DS2CTC_DENSE_THREADS 256
+#endif
+constexpr int kDenseThreads = DS2CTC_DENSE_THREADS;
 
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
@@ -73,7 +75,32 @@ __device__ __forceinline__ float block_sum(float v, float* sh) {
   return s;
 }
 
-__global__ void __launch_bounds__(kDenseThreads) k_dense(PairArgs a, int write_grad) {
+// Resident blocks per SM the register budget is sized for: the row lives in
+// VEC float4 registers per thread, and more resident rows per SM keep more
+// loads in flight while other blocks sit in their reductions (k_dense at
+// 58 registers, 4 blocks: 61 % of HBM peak in round 1).
+// (~4 VEC + 26 registers per thread without spills; DS2CTC_DENSE_MINB forces it)
+constexpr int dense_min_blocks(int vec) {
+#ifdef DS2CTC_DENSE_MINB
+  return vec > 0 ? DS2CTC_DENSE_MINB : 1;
+#else
+  const int regs = (4 * vec + 26 + 7) / 8 * 8;
+  const int by_regs = 65536 / (kDenseThreads * regs), by_threads = 2048 / kDenseThreads;
+  return vec == 0 ? 1 : by_regs < 1 ? 1 : by_regs < by_threads ? by_regs : by_threads;
+#endif
+}
+
+// One CTA per frame row (t, b). VEC > 0: the row (A/4 float4, A % 4 == 0,
+// A <= 4 * kDenseThreads * VEC) stays in registers between the statistics and the store,
+// exp evaluated once per element: one HBM read, one HBM write. VEC == 0: the
+// generic two-pass form (the second pass hits L1/L2).
+//  SOFT == false (k_dense): after k_pair; rows of lattices without mass are
+//    zeroed, and the key-column occupancies are subtracted from the row just
+//    written (grad_column, ctc.cpp:69-79).
+//  SOFT == true (k_dense_soft): needs nothing from k_pair, so it can run
+//    concurrently with it; k_dense_patch subtracts the occupancies afterwards.
+template <int VEC, bool SOFT>
+__global__ void __launch_bounds__(kDenseThreads, dense_min_blocks(VEC)) k_dense_t(PairArgs a, int write_grad) {
   __shared__ float sh[32];
   const int row = blockIdx.x;
   const int t = row / a.B;
@@ -83,21 +110,20 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense(PairArgs a, int write_g
   const int tid = threadIdx.x;
   float* gr = write_grad ? a.grad + static_cast<size_t>(row) * A : nullptr;
   const float* xr = a.x + static_cast<size_t>(row) * A;
-  const bool live = u.status == 0 && t < u.T && a.logz[b] != -__builtin_huge_val();
+  const bool live = u.status == 0 && t < u.T && (SOFT || a.logz[b] != -__builtin_huge_val());
   if (!live) {
     if (gr)
       for (int c = tid; c < A; c += kDenseThreads) gr[c] = 0.f;
     return;
   }
-  const bool vec = (A & 3) == 0 && A <= kDenseVec * kDenseThreads * 4;
   float m, ls;
-  if (vec) {  // the row stays in registers: one HBM read, one HBM write
+  if constexpr (VEC > 0) {
     const int n4 = A >> 2;
     const float4* x4 = reinterpret_cast<const float4*>(xr);
-    float4 v[kDenseVec];
+    float4 v[VEC];
     m = -__builtin_huge_valf();
 #pragma unroll
-    for (int j = 0; j < kDenseVec; ++j) {
+    for (int j = 0; j < VEC; ++j) {
       const int q = tid + j * kDenseThreads;
       v[j] = q < n4 ? ldg_stream(x4 + q) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
       m = fmaxf(m, fmaxf(fmaxf(v[j].x, v[j].y), fmaxf(v[j].z, v[j].w)));
@@ -105,22 +131,22 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense(PairArgs a, int write_g
     m = block_max(m, sh);
     float s = 0.f;
 #pragma unroll
-    for (int j = 0; j < kDenseVec; ++j)
-      s += (__expf(v[j].x - m) + __expf(v[j].y - m)) + (__expf(v[j].z - m) + __expf(v[j].w - m));
+    for (int j = 0; j < VEC; ++j) {
+      v[j] = make_float4(__expf(v[j].x - m), __expf(v[j].y - m), __expf(v[j].z - m), __expf(v[j].w - m));
+      s += (v[j].x + v[j].y) + (v[j].z + v[j].w);
+    }
     s = block_sum(s, sh);
     ls = logf(s);
     if (gr) {
       float4* g4 = reinterpret_cast<float4*>(gr);
-      const float off = m + ls;
+      const float inv = 1.f / s;
 #pragma unroll
-      for (int j = 0; j < kDenseVec; ++j) {
+      for (int j = 0; j < VEC; ++j) {
         const int q = tid + j * kDenseThreads;
-        if (q < n4)
-          stg_stream(g4 + q, make_float4(__expf(v[j].x - off), __expf(v[j].y - off), __expf(v[j].z - off),
-                                         __expf(v[j].w - off)));
+        if (q < n4) stg_stream(g4 + q, make_float4(v[j].x * inv, v[j].y * inv, v[j].z * inv, v[j].w * inv));
       }
     }
-  } else {  // generic: two passes (the second hits L1/L2)
+  } else {
     m = -__builtin_huge_valf();
     for (int c = tid; c < A; c += kDenseThreads) m = fmaxf(m, __ldg(xr + c));
     m = block_max(m, sh);
@@ -132,7 +158,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense(PairArgs a, int write_g
       for (int c = tid; c < A; c += kDenseThreads) gr[c] = __expf(__ldg(xr + c) - (m + ls));
   }
   if (tid == 0) a.lse[row] = make_float2(m, ls);
-  if (!gr) return;
+  if (SOFT || !gr) return;
   // Occupancy of the utterance's key symbols (<= L + 1 distinct symbols per
   // row, the key map of group_rows_by_key, ctc.cpp:47-66): read-modify-write
   // of the row just written (visible to the block after the barrier; the
@@ -146,75 +172,39 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense(PairArgs a, int write_g
   }
 }
 
-// The HBM pass split in two so that its bulk overlaps k_pair (which leaves the
-// memory system idle for ~110 us at the Mandarin shape, while its one CTA
-// per SM leaves room for more):
-//  k_dense_soft  -- needs nothing from k_pair: per (t, b) row the max and the
-//                   log-sum-exp (log_softmax_rows, ctc.cpp:24-37) and the
-//                   softmax row written to the gradient, exp evaluated once
-//                   per element (kept in registers between the sum and the
-//                   store). Runs on a forked stream concurrently with k_pair.
-//  k_dense_patch -- after k_pair: subtract the occupancies at the <= L + 1
-//                   key columns of each row (grad_column, ctc.cpp:69-79), and
-//                   zero the rows of utterances whose lattice has no mass.
-__global__ void __launch_bounds__(kDenseThreads) k_dense_soft(PairArgs a, int write_grad) {
-  __shared__ float sh[32];
-  const int row = blockIdx.x;
-  const int t = row / a.B;
-  const int b = row - t * a.B;
-  const UttDesc u = a.desc[b];
-  const int A = a.A;
-  const int tid = threadIdx.x;
-  float* gr = write_grad ? a.grad + static_cast<size_t>(row) * A : nullptr;
-  const float* xr = a.x + static_cast<size_t>(row) * A;
-  if (!(u.status == 0 && t < u.T)) {
-    if (gr)
-      for (int c = tid; c < A; c += kDenseThreads) gr[c] = 0.f;
-    return;
+// float4 registers per thread for a row of A logits (0: the generic path).
+int dense_vec(int A) {
+  if ((A & 3) != 0) return 0;
+  const int v = (A / 4 + kDenseThreads - 1) / kDenseThreads;
+  return v <= 8 ? v : 0;
+}
+
+template <int VEC, bool SOFT>
+cudaError_t launch_dense_v(const PairArgs& a, int wg, int smem, cudaStream_t s) {
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(k_dense_t<VEC, SOFT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
   }
-  const bool vec = (A & 3) == 0 && A <= kDenseVec * kDenseThreads * 4;
-  float m, ls;
-  if (vec) {  // the row stays in registers: one HBM read, one HBM write
-    const int n4 = A >> 2;
-    const float4* x4 = reinterpret_cast<const float4*>(xr);
-    float4 v[kDenseVec];
-    m = -__builtin_huge_valf();
-#pragma unroll
-    for (int j = 0; j < kDenseVec; ++j) {
-      const int q = tid + j * kDenseThreads;
-      v[j] = q < n4 ? ldg_stream(x4 + q) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-      m = fmaxf(m, fmaxf(fmaxf(v[j].x, v[j].y), fmaxf(v[j].z, v[j].w)));
-    }
-    m = block_max(m, sh);
-    float s = 0.f;
-#pragma unroll
-    for (int j = 0; j < kDenseVec; ++j) {
-      v[j] = make_float4(__expf(v[j].x - m), __expf(v[j].y - m), __expf(v[j].z - m), __expf(v[j].w - m));
-      s += (v[j].x + v[j].y) + (v[j].z + v[j].w);
-    }
-    s = block_sum(s, sh);
-    ls = logf(s);
-    if (gr) {
-      float4* g4 = reinterpret_cast<float4*>(gr);
-      const float inv = 1.f / s;
-#pragma unroll
-      for (int j = 0; j < kDenseVec; ++j) {
-        const int q = tid + j * kDenseThreads;
-        if (q < n4) stg_stream(g4 + q, make_float4(v[j].x * inv, v[j].y * inv, v[j].z * inv, v[j].w * inv));
-      }
-    }
-  } else {  // generic: two passes (the second hits L1/L2)
-    m = -__builtin_huge_valf();
-    for (int c = tid; c < A; c += kDenseThreads) m = fmaxf(m, __ldg(xr + c));
-    m = block_max(m, sh);
-    float s = 0.f;
-    for (int c = tid; c < A; c += kDenseThreads) s += __expf(__ldg(xr + c) - m);
-    s = block_sum(s, sh);
-    ls = logf(s);
-    if (gr)
-      for (int c = tid; c < A; c += kDenseThreads) gr[c] = __expf(__ldg(xr + c) - (m + ls));
+  const unsigned rows = static_cast<unsigned>(static_cast<long long>(a.t_max) * a.B);
+  k_dense_t<VEC, SOFT><<<rows, kDenseThreads, static_cast<size_t>(smem), s>>>(a, wg);
+  return cudaGetLastError();
+}
+
+template <bool SOFT>
+int launch_dense_rows(const PairArgs& a, bool write_grad, int smem, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int wg = write_grad ? 1 : 0;
+  switch (dense_vec(a.A)) {
+    case 1: return launch_dense_v<1, SOFT>(a, wg, smem, s);
+    case 2: return launch_dense_v<2, SOFT>(a, wg, smem, s);
+    case 3: return launch_dense_v<3, SOFT>(a, wg, smem, s);
+    case 4: return launch_dense_v<4, SOFT>(a, wg, smem, s);
+    case 5: return launch_dense_v<5, SOFT>(a, wg, smem, s);
+    case 6: return launch_dense_v<6, SOFT>(a, wg, smem, s);
+    case 7: return launch_dense_v<7, SOFT>(a, wg, smem, s);
+    case 8: return launch_dense_v<8, SOFT>(a, wg, smem, s);
+    default: return launch_dense_v<0, SOFT>(a, wg, smem, s);
   }
-  if (tid == 0) a.lse[row] = make_float2(m, ls);
 }
 
 // One warp per (t, b) row.
@@ -236,26 +226,35 @@ __global__ void k_dense_patch(PairArgs a) {
   for (int j = lane; j < u.nkey; j += 32) gr[keys[j]] -= occ[j];
 }
 
-// costs[b] = sum_t lse_t - log Z (natural log), one warp per utterance.
-// log Z = log Z' + sum_t mk_t, with log Z' (log2 units) from k_pair.
-__global__ void k_finalize(PairArgs a) {
-  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (b >= a.B) return;
+// costs[b] = sum_t lse_t - log Z (natural log), one block per utterance: the
+// lse column of utterance b is strided by B in memory, so 256 threads keep
+// ~T/256 independent loads each in flight (one warp per utterance left each
+// lane ~T/32 strided loads deep: 11 us at the Mandarin shape). Fixed
+// per-thread order, then a fixed tree: deterministic.
+constexpr int kFinalizeThreads = 256;
+__global__ void __launch_bounds__(kFinalizeThreads) k_finalize(PairArgs a) {
+  __shared__ double sh[kFinalizeThreads / 32];
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const UttDesc u = a.desc[b];
   if (u.status != 0) {
-    if (lane == 0) a.costs[b] = u.status == 2 ? 0.f : __builtin_huge_valf();
+    if (tid == 0) a.costs[b] = u.status == 2 ? 0.f : __builtin_huge_valf();
     return;
   }
   const double lz = a.logz[b];
   double acc = 0.0;
-  for (int t = lane; t < u.T; t += 32) {
+  for (int t = tid; t < u.T; t += kFinalizeThreads) {
     const float2 v = a.lse[static_cast<size_t>(t) * a.B + b];
     acc += static_cast<double>(v.x) + static_cast<double>(v.y);
   }
   acc = warp_sum_d(acc);
+  if (lane == 0) sh[warp] = acc;
+  __syncthreads();
+  acc = 0.0;
+#pragma unroll
+  for (int w = 0; w < kFinalizeThreads / 32; ++w) acc += sh[w];
   // k_pair ran on frames shifted by mk_t and left -sum_t mk_t in part[2b], part[2b+1].
-  if (lane == 0)
+  if (tid == 0)
     a.costs[b] = lz == -__builtin_huge_val()
                      ? __builtin_huge_valf()
                      : static_cast<float>((acc + (a.part[2 * b] + a.part[2 * b + 1])) - lz * kLn2);
@@ -266,7 +265,7 @@ __global__ void k_finalize(PairArgs a) {
   if (a.grad != nullptr && acc != acc && lz != -__builtin_huge_val()) {
     const float qnan = __int_as_float(0x7fc00000);
     const int* keys = a.key_char + u.key_off;
-    for (int t = lane; t < u.T; t += 32) {
+    for (int t = tid; t < u.T; t += kFinalizeThreads) {
       float* gr = a.grad + (static_cast<size_t>(t) * a.B + b) * a.A;
       for (int j = 0; j < u.nkey; ++j) gr[keys[j]] = qnan;
     }
@@ -295,18 +294,19 @@ __global__ void k_loss_sum(const float* __restrict__ costs, int B, double* __res
 }  // namespace
 
 int launch_dense(const PairArgs& a, bool write_grad, void* stream) {
-  const long long rows = static_cast<long long>(a.t_max) * a.B;
-  if (rows == 0) return cudaSuccess;
-  k_dense<<<static_cast<unsigned>(rows), kDenseThreads, 0, static_cast<cudaStream_t>(stream)>>>(a, write_grad ? 1 : 0);
-  return cudaGetLastError();
+  if (static_cast<long long>(a.t_max) * a.B == 0) return cudaSuccess;
+  return launch_dense_rows<false>(a, write_grad, 0, stream);
 }
 
-int launch_dense_soft(const PairArgs& a, bool write_grad, void* stream) {
-  const long long rows = static_cast<long long>(a.t_max) * a.B;
-  if (rows == 0) return cudaSuccess;
-  k_dense_soft<<<static_cast<unsigned>(rows), kDenseThreads, 0, static_cast<cudaStream_t>(stream)>>>(a,
-                                                                                                    write_grad ? 1 : 0);
-  return cudaGetLastError();
+// The HBM pass split in two so that its bulk overlaps k_pair (latency-bound,
+// HBM idle): k_dense_soft (statistics + softmax rows) on a forked stream
+// concurrently with k_pair, k_dense_patch (key-column occupancies) after both.
+// exclude_smem > 0: a dynamic shared-memory request (unused) sized so that no
+// k_dense_soft block fits next to a k_pair CTA (opt-in; measured slower,
+// DESIGN.md section 5.2).
+int launch_dense_soft(const PairArgs& a, bool write_grad, int exclude_smem, void* stream) {
+  if (static_cast<long long>(a.t_max) * a.B == 0) return cudaSuccess;
+  return launch_dense_rows<true>(a, write_grad, exclude_smem, stream);
 }
 
 int launch_dense_patch(const PairArgs& a, void* stream) {
@@ -318,7 +318,7 @@ int launch_dense_patch(const PairArgs& a, void* stream) {
 
 int launch_finalize(const PairArgs& a, void* stream) {
   if (a.B == 0) return cudaSuccess;
-  k_finalize<<<(a.B + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  k_finalize<<<a.B, kFinalizeThreads, 0, static_cast<cudaStream_t>(stream)>>>(a);
   return cudaGetLastError();
 }
 

@@ -300,7 +300,7 @@ int launch_pair_k8(const PairArgs& a, void* stream);  // ctc_pair_k8.cu
 int read_watchdog_k8(unsigned long long* out4);
 int launch_dense(const PairArgs& a, bool write_grad, void* stream);
 int launch_finalize(const PairArgs& a, void* stream);
-int launch_dense_soft(const PairArgs& a, bool write_grad, void* stream);
+int launch_dense_soft(const PairArgs& a, bool write_grad, int exclude_smem, void* stream);
 int launch_dense_patch(const PairArgs& a, void* stream);
 int launch_loss_sum(const float* costs, int B, double* out2, void* stream);
 

@@ -3,7 +3,7 @@ each workload's dominant kernel from one ncu capture, stamped with the content
 hash of the library build it was measured on (libds2ctc.so.sha256), which
 bench.py checks before reporting it as roofline.traffic. Run on the GPU box:
 
-    python tools/ncu/traffic.py english:k_pair mandarin:k_dense_soft
+    python tools/ncu/traffic.py english:k_pair mandarin:k_dense_t
 """
 import csv
 import json

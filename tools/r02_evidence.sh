@@ -8,9 +8,9 @@ for w in english mandarin sortagrad english-step config1 edge1500; do
 done
 timeout 200 python bench.py --impl reference --steps 3 --warmup 1 > $O/ref_english.json 2> $O/ref_english.err
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_pair -s 3 -c 1 -o $O/k_pair_english python bench.py --steps 1 --warmup 3 --no-cpu-baseline --soak-seconds 0 > $O/ncu1.log 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_dense_soft -s 2 -c 1 -o $O/k_dense_soft_mandarin python bench.py --workload mandarin --steps 1 --warmup 3 --no-cpu-baseline --soak-seconds 0 > $O/ncu2.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_dense_t -s 2 -c 1 -o $O/k_dense_mandarin python bench.py --workload mandarin --steps 1 --warmup 3 --no-cpu-baseline --soak-seconds 0 > $O/ncu2.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_fc_gemm -c 2 -o $O/k_fc_gemm_step python bench.py --workload english-step --steps 1 --warmup 3 --no-cpu-baseline --soak-seconds 0 > $O/ncu3.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_english.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --soak-seconds 0 > /dev/null 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_step.csv python bench.py --workload english-step --steps 2 --warmup 3 --no-cpu-baseline --soak-seconds 0 > /dev/null 2>&1
-timeout 900 python tools/ncu/traffic.py english:k_pair mandarin:k_dense_soft english-step:k_pair > $O/traffic.log 2>&1
+timeout 900 python tools/ncu/traffic.py english:k_pair mandarin:k_dense_t english-step:k_pair > $O/traffic.log 2>&1
 cp profiles/ncu_traffic.json $O/ncu_traffic.json

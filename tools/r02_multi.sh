@@ -1,8 +1,14 @@
+# Multi-GPU evidence on one box: gpu multi tests, then bench lines at N=1,2,..,NGPU.
 set -u
 O=gpurun_out/${TAG:-r02m2}; mkdir -p $O
 N=${NGPU:-2}
 nvidia-smi -L > $O/gpus.txt
 timeout 600 python -m pytest tests/test_gpu_multi.py -m gpu -x -q -s > $O/pytest_multi.log 2>&1; echo PYTEST $? >> $O/pytest_multi.log
 for w in english sortagrad english-step; do
-  timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus $N --workload $w --steps 30 --warmup 5 > $O/b${N}_$w.json 2> $O/b${N}_$w.err
+  timeout 300 python bench.py --workload $w --steps 30 --warmup 5 --cpu-seconds 3 > $O/b1_$w.json 2> $O/b1_$w.err
+  n=2
+  while [ $n -le $N ]; do
+    timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus $n --workload $w --steps 30 --warmup 5 > $O/b${n}_$w.json 2> $O/b${n}_$w.err
+    n=$((n * 2))
+  done
 done
