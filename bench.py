@@ -357,7 +357,7 @@ def main():
         if not torch.allclose(pair, ref_pair, rtol=1e-12, atol=0):
             raise RuntimeError(f"peer all-reduce {pair.tolist()} != NCCL {ref_pair.tolist()}")
 
-    dense_overlap = os.environ.get("DS2CTC_DENSE_OVERLAP", "1") != "0"  # the library's default (ctc_api.cpp)
+    dense_overlap = os.environ.get("DS2CTC_DENSE_OVERLAP", "0") != "0"  # the library's default (ctc_api.cpp): off
     # kernels of ours per step: k_pair (+ k_dense + k_finalize for large A) + k_loss_sum / k_loss_allreduce
     if B:
         # large A: k_dense + k_finalize, or (overlapped) k_dense_soft + k_dense_patch + k_finalize

@@ -253,12 +253,17 @@ std::pair<int, int> build_metadata(const Layout& lay, const int* flat_labels, co
   return {max_L, max_nkey};
 }
 
-// DS2CTC_DENSE_OVERLAP=0: the large-alphabet HBM pass after k_pair (one
-// kernel) instead of concurrently with it (default on).
+// DS2CTC_DENSE_OVERLAP=1: the large-alphabet HBM pass split into k_dense_soft
+// (concurrently with k_pair, on a forked stream) + k_dense_patch, instead of
+// one k_dense after k_pair. Opt-in: with the register-resident row evaluated
+// once per element, the serial pass measures faster (Mandarin 329 vs 337 us
+// per step, profiles/r02_dense_ab.txt): co-resident dense blocks slow the chains
+// (k_pair 122 -> 127 us), fit only ~2 per k_pair SM, and the patch re-reads
+// the key columns.
 bool dense_overlap_enabled() {
   static const bool on = [] {
     const char* v = std::getenv("DS2CTC_DENSE_OVERLAP");
-    return v == nullptr || std::atoi(v) != 0;
+    return v != nullptr && std::atoi(v) != 0;
   }();
   return on;
 }
@@ -273,7 +278,7 @@ bool dense_overlap_enabled() {
 // Opt-in (DS2CTC_DENSE_EXCLUDE=1): measured slower, 370 vs 345 us per
 // Mandarin step -- the 20 SMs k_pair leaves free move too little of the pass
 // and the request caps the later full-GPU part at 4 blocks per SM
-// (gpurun_out/r02mand).
+// (profiles/r02_dense_ab.txt).
 int dense_exclusion_smem(const Geometry& g) {
   static const bool on = [] {
     const char* v = std::getenv("DS2CTC_DENSE_EXCLUDE");
@@ -597,6 +602,8 @@ struct HostContext {
   size_t ws_cap = 0;
   // extra streams of the chunked host pipeline (ds2ctc_compute_loss_host)
   cudaStream_t chunk_streams[kHostChunksMax - 1] = {};
+  // end of chunk c's activation upload: chunk c + 1's upload waits for it
+  cudaEvent_t uploaded[kHostChunksMax] = {};
   ~HostContext() {
     if (device < 0) return;
     cudaSetDevice(device);
@@ -607,6 +614,8 @@ struct HostContext {
     if (stream) cudaStreamDestroy(stream);
     for (cudaStream_t cs : chunk_streams)
       if (cs) cudaStreamDestroy(cs);
+    for (cudaEvent_t ev : uploaded)
+      if (ev) cudaEventDestroy(ev);
   }
 };
 
@@ -1053,6 +1062,18 @@ ds2ctc_status ds2ctc_compute_loss_host(const float* activations, float* gradient
     if (!ctx.chunk_streams[c - 1] &&
         cudaStreamCreateWithFlags(&ctx.chunk_streams[c - 1], cudaStreamNonBlocking) != cudaSuccess)
       return DS2CTC_STATUS_EXECUTION_FAILED;
+  for (int c = 0; c + 1 < nc; ++c)
+    if (!ctx.uploaded[c] && cudaEventCreateWithFlags(&ctx.uploaded[c], cudaEventDisableTiming) != cudaSuccess)
+      return DS2CTC_STATUS_EXECUTION_FAILED;
+  // Uploads in chunk order, one at a time (DS2CTC_HOST_SERIAL_UPLOAD=0: all at
+  // once). Issued concurrently, the chunks' copies share PCIe and all land at
+  // the end of the whole upload, so every chunk's kernels start late; one at a
+  // time, chunk 0's k_pair starts after a quarter of it and only the last
+  // chunk's kernels trail the upload.
+  static const bool serial_upload = [] {
+    const char* v = std::getenv("DS2CTC_HOST_SERIAL_UPLOAD");
+    return v == nullptr || std::atoi(v) != 0;
+  }();
 
   const size_t row = static_cast<size_t>(B) * A * sizeof(float);
   // The contract is synchronous: on an error after some chunk was enqueued,
@@ -1074,9 +1095,13 @@ ds2ctc_status ds2ctc_compute_loss_host(const float* activations, float* gradient
                : direct   ? reinterpret_cast<unsigned char*>(g_direct) + x_off[c]
                           : static_cast<unsigned char*>(ctx.grads) + x_off[c];
     const auto* xh = reinterpret_cast<const unsigned char*>(activations) + static_cast<size_t>(b0[c]) * A * sizeof(float);
+    if (serial_upload && c > 0 && cudaStreamWaitEvent(sc, ctx.uploaded[c - 1], 0) != cudaSuccess)
+      return drain(DS2CTC_STATUS_EXECUTION_FAILED);
     if (t_c[c] > 0 && w > 0 &&
         cudaMemcpy2DAsync(xd, xpitch, xh, row, w, t_c[c], cudaMemcpyHostToDevice, sc) != cudaSuccess)
       return drain(DS2CTC_STATUS_MEMOPS_FAILED);
+    if (serial_upload && c + 1 < nc && cudaEventRecord(ctx.uploaded[c], sc) != cudaSuccess)
+      return drain(DS2CTC_STATUS_EXECUTION_FAILED);
     float* cd = static_cast<float*>(ctx.costs) + b0[c];
     st = run(reinterpret_cast<const float*>(xd), reinterpret_cast<float*>(gd), flat_labels + lab0[c],
              label_lengths + b0[c], input_lengths + b0[c], A, bc, blank_label, cd,

@@ -310,6 +310,23 @@ def test_host_api_direct_mode(cuda):
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 
+def test_dense_overlap_mode(cuda):
+    # the opt-in overlapped large-alphabet pass (k_dense_soft on a forked stream
+    # concurrently with k_pair, then k_dense_patch) is read once per process:
+    # rerun the large-alphabet parity cases (Mandarin B = 64, NaN/inf rows at
+    # A = 200, cost-only) in a child process with it switched on
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, DS2CTC_DENSE_OVERLAP="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        f"{__file__}::test_fixed_shapes_vs_oracle[shape1]",
+                        f"{__file__}::test_nan_inf_rows_match_reference[200]", f"{__file__}::test_cost_only_matches"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "passed" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 def test_fused_loss_allreduce_single_rank(cuda):
     # ds2ctc_loss_sum_allreduce with world = 1 (its own mailbox) equals ds2ctc_loss_sum;
     # the multi-rank path is checked against NCCL inside bench.py at N > 1

@@ -3,8 +3,8 @@ set -u
 O=gpurun_out/${TAG:-r02m2}; mkdir -p $O
 N=${NGPU:-2}
 nvidia-smi -L > $O/gpus.txt
-timeout 600 python -m pytest tests/test_gpu_multi.py -m gpu -x -q -s > $O/pytest_multi.log 2>&1; echo PYTEST $? >> $O/pytest_multi.log
-for w in english sortagrad english-step; do
+timeout 1200 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo PYTEST $? >> $O/pytest_gpu.log
+for w in ${WORKLOADS:-english sortagrad english-step}; do
   timeout 300 python bench.py --workload $w --steps 30 --warmup 5 --cpu-seconds 3 > $O/b1_$w.json 2> $O/b1_$w.err
   n=2
   while [ $n -le $N ]; do
