@@ -15,11 +15,12 @@
 // Both products run on the 5th-generation tensor cores: one thread issues
 // tcgen05.mma (kind::tf32, fp32 accumulators in TMEM) on 128 x 128 tiles
 // whose operands TMA streams into 128B-swizzled shared memory through a
-// 4-stage mbarrier pipeline; four epilogue warps read the accumulators back
+// 1-4 stage mbarrier pipeline; four epilogue warps read the accumulators back
 // with tcgen05.ld and store them (dx) or add them (dW, split over the rows:
-// the contraction dimension is the T*B rows). K-major operands (dpre in dx)
-// and MN-major operands (dpre^T and x in dW, W in dx) are both native
-// tcgen05 layouts, so nothing is transposed in memory.
+// the contraction dimension is the T*B rows). tcgen05 kind::tf32 reads
+// K-major operands only, so the MN-major operands of dW (dpre^T and x) are
+// transposed per stage in shared memory by the epilogue warps, and W for dx
+// is transposed once into the workspace.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -156,6 +157,11 @@ __device__ __forceinline__ uint64_t tile_desc(const float* tile, int j) {
   return smem_desc(reinterpret_cast<const char*>(tile) + 32 * j, 16, 1024);
 }
 
+// Epilogue staging row pitch (floats): 16-byte aligned rows whose float4
+// writes (a quarter-warp per row) and float4 reads (a quarter-warp per row)
+// hit distinct banks.
+constexpr int kOutPitch = 36;
+
 struct GemmArgs {
   int M, N;          // extent of D (M x N)
   int k_blocks;      // 32-wide K blocks per split
@@ -168,7 +174,7 @@ struct GemmArgs {
 
 template <bool kAMN, bool kBMN, int BN, int STAGES>
 __host__ __device__ constexpr int gemm_smem() {
-  return STAGES * ((kTileBytes + BN * kTileK * 4) * (1 + (kAMN || kBMN))) + 4 * 32 * 33 * 4 + 256 + 1024;
+  return STAGES * ((kTileBytes + BN * kTileK * 4) * (1 + (kAMN || kBMN))) + 4 * 32 * kOutPitch * 4 + 256 + 1024;
 }
 
 // D[M x N] (+)= A[M x K] . B[K x N]; blockIdx = (n tile, m tile, K split).
@@ -191,8 +197,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (kAMN) p += kStages * kTileBytes;
   float* b_raw = reinterpret_cast<float*>(p);
   if (kBMN) p += kStages * kBBytes;
-  float* stage_out = reinterpret_cast<float*>(p);  // [4 warps][32][33]
-  uint64_t* full = reinterpret_cast<uint64_t*>(p + 4 * 32 * 33 * 4);
+  float* stage_out = reinterpret_cast<float*>(p);  // [4 warps][32][kOutPitch]
+  uint64_t* full = reinterpret_cast<uint64_t*>(p + 4 * 32 * kOutPitch * 4);
   uint64_t* ready = full + kStages;   // transposed (MN-major operands only)
   uint64_t* empty = ready + kStages;
   uint64_t* done = empty + kStages;
@@ -266,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int q = warp & 3;  // TMEM lane quarter this warp may access
       mbar_wait(done, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      float* buf = stage_out + (warp - 2) * 32 * 33;
+      float* buf = stage_out + (warp - 2) * 32 * kOutPitch;
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t v[32];
         const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c0);
@@ -294,17 +300,35 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           continue;
         }
+        // lane = row: its 32 columns into the staging rows as float4; then a
+        // quarter-warp per row reads them back as float4, so each store
+        // instruction writes four full 128-byte row segments
 #pragma unroll
-        for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = __uint_as_float(v[j]);
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(buf + lane * kOutPitch + j) =
+              make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
+                          __uint_as_float(v[j + 3]));
         __syncwarp();
-        const int col = n0 + c0 + lane;
-        for (int r = 0; r < 32; ++r) {
+        const int c4 = (lane & 7) * 4;
+        const int col = n0 + c0 + c4;
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int r = it * 4 + (lane >> 3);
           const int row = m0 + q * 32 + r;
-          if (row < g.M && col < g.N) {
+          const float4 val = *reinterpret_cast<const float4*>(buf + r * kOutPitch + c4);
+          if (row < g.M) {
             float* o = g.out + static_cast<long long>(row) * g.ldo + col;
-            const float val = buf[r * 33 + lane];
-            if (g.accumulate) atomicAdd(o, val);
-            else *o = val;
+            if (col + 3 < g.N && !g.accumulate) {
+              *reinterpret_cast<float4*>(o) = val;  // ldo % 4 == 0 and a 16-byte aligned base (validated)
+            } else {
+              const float e[4] = {val.x, val.y, val.z, val.w};
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (col + u < g.N) {
+                  if (g.accumulate) atomicAdd(o + u, e[u]);
+                  else o[u] = e[u];
+                }
+            }
           }
         }
         __syncwarp();
@@ -406,6 +430,7 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& g,
   int dev = 0;
   cudaGetDevice(&dev);
   constexpr int smem = gemm_smem<kAMN, kBMN, BN, STAGES>();
+  static_assert(smem <= 232448, "k_fc_gemm stage rings exceed the 227 KB shared-memory opt-in");
   if (dev >= 0 && dev < 64 && !configured[dev]) {
     cudaError_t e = cudaFuncSetAttribute(k_fc_gemm<kAMN, kBMN, BN, STAGES>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -468,9 +493,24 @@ int fc_backward(const float* g, const float* x, const float* w, float* dw, float
   if (dw) {
     CUtensorMap ma, mb;
     const int kb = (rows + kTileK - 1) / kTileK;
+    // K split: whole waves of the one-CTA-per-SM grid (a partial last wave
+    // costs a full one: 20 tiles x 30 splits = 600 CTAs was 4.05 waves),
+    // 2-5 waves, the fullest last wave winning (English dW 131 -> 118 us)
     auto split_for = [&](int tiles) {
-      const int sp = std::max(1, std::min(kb, (4 * sm_count + tiles - 1) / tiles));
-      const int kpb = (kb + sp - 1) / sp;
+      int best_sp = 1;
+      double best_eff = -1.0;
+      for (int w = 2; w <= 5; ++w) {
+        const int sp = std::max(1, std::min(kb, w * sm_count / tiles));
+        const int kpb = (kb + sp - 1) / sp;
+        const int n = (kb + kpb - 1) / kpb;  // splits actually launched
+        const long long ctas = static_cast<long long>(n) * tiles;
+        const double eff = static_cast<double>(ctas) / (((ctas + sm_count - 1) / sm_count) * sm_count);
+        if (eff > best_eff + 1e-9) {
+          best_eff = eff;
+          best_sp = sp;
+        }
+      }
+      const int kpb = (kb + best_sp - 1) / best_sp;
       return std::make_pair((kb + kpb - 1) / kpb, kpb);
     };
     int e;
