@@ -554,6 +554,24 @@ def main():
             "e2e": {"value": total_utts / (e2e_ms / 1e3), "unit": UNIT,
                     "h2d_bytes_per_step": int(acts_h.nbytes + 4 * (ll.sum() + 2 * B)),
                     "d2h_bytes_per_step": int(acts_h.nbytes + 4 * B), "ms_per_step": e2e_ms},
+            # north_star (1): the log-softmax over the alphabet (log_softmax_rows, ctc.cpp:24-37).
+            # Large alphabets: it is the dense pass itself (row max + log-sum-exp, the softmax
+            # row written with the gradient), reported as achieved GB/s. Small ones: fused
+            # into k_pair's service warp (the logits are staged once, per epoch, while the
+            # chain runs; epoch timing shows it off the critical path: DESIGN.md section 5.1),
+            # so it has no launch or GB/s of its own.
+            "log_softmax": ({"kernel": dense_name, "ms": dense_ms,
+                             "bytes": 8.0 * float((il.astype(np.float64) * A).sum()),
+                             "achieved_gbs": 8.0 * float((il.astype(np.float64) * A).sum()) / (dense_ms / 1e3) / 1e9
+                             if dense_ms > 0 else 0.0,
+                             "frac": (8.0 * float((il.astype(np.float64) * A).sum()) / (dense_ms / 1e3) / 1e9) / peak
+                             if dense_ms > 0 else 0.0,
+                             "loads": "float4 rows, L1 no-allocate; block max / sum by warp shuffles"}
+                            if A > 128 else
+                            {"kernel": "fused into k_pair (service warp)", "bytes_read": 4.0 * float(
+                                (il.astype(np.float64) * A).sum()),
+                             "note": "one coalesced row read per frame, max / log-sum-exp in the same pass; "
+                                     "latency-hidden behind the lattice chain, no separate HBM pass"}),
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
             "loss_sum": loss_sum, "skipped": int(skipped),

@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cmath>
 #include <limits>
+#include <ostream>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -188,6 +189,26 @@ CtcLattice<M> ctc_lattice_gpu(const M& frame_logits, const std::vector<int>& lab
       lat.beta(s, t) = b[static_cast<size_t>(s) * T + t];
     }
   return lat;
+}
+
+// dump_lattice_tsv (ctc.cpp:372-383, declared ctc.hpp:104-105): for "alpha"
+// then "beta", a header line "# <name> (<rows> x <cols>)" and one line per
+// augmented position -- its symbol, then the row's values tab-separated, in
+// the stream's current number format. Takes ds2ctc::CtcLattice or any lattice
+// type with the same fields (asr::ctc::CtcLattice), so the debug printer
+// works on what ctc_lattice_gpu returns without the reference library.
+template <class Lattice>
+void dump_lattice_tsv(const Lattice& lat, std::ostream& os) {
+  auto one = [&](const char* name, const auto& m) {
+    os << "# " << name << " (" << m.rows() << " x " << m.cols() << ")\n";
+    for (int s = 0; s < m.rows(); ++s) {
+      os << lat.augmented_label[static_cast<size_t>(s)];
+      for (int t = 0; t < m.cols(); ++t) os << '\t' << m(s, t);
+      os << '\n';
+    }
+  };
+  one("alpha", lat.alpha);
+  one("beta", lat.beta);
 }
 
 }  // namespace ds2ctc

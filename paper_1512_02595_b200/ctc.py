@@ -269,6 +269,18 @@ def ctc_lattice(frame_logits, label: Sequence[int], blank: int, device: int = 0)
     return CtcLattice(aug, alpha.cpu().numpy().reshape(S, T), beta.cpu().numpy().reshape(S, T), float(lp[0].item()))
 
 
+def dump_lattice_tsv(lat: CtcLattice, out) -> None:
+    """dump_lattice_tsv (ctc.cpp:372-383): for "alpha" then "beta", a header
+    "# <name> (<rows> x <cols>)" and one line per augmented position -- its
+    symbol, then the row's values tab-separated in C++ default stream format
+    (6 significant digits, "%g")."""
+    for name, m in (("alpha", lat.alpha), ("beta", lat.beta)):
+        m = np.asarray(m)
+        out.write(f"# {name} ({m.shape[0]} x {m.shape[1]})\n")
+        for s in range(m.shape[0]):
+            out.write(str(int(lat.augmented_label[s])) + "".join("\t" + format(float(v), "g") for v in m[s]) + "\n")
+
+
 def fc_backward(dlogits, x, w, dw=None, db=None, dx=None, want_dx: bool = True, stream=None,
                 workspace: Optional[Workspace] = None):
     """The output layer's backward pass on the CTC gradient, on the device

@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdio>
 #include <set>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -179,6 +180,22 @@ int main() {
         }
       check(close_rel(lat.log_prob, ref.log_prob, 1e-12), "lattice log p " + std::to_string(it));
     }
+  }
+  // test_ctc.cpp:277-284 -- lattice TSV dump: the reference's printer and the
+  // shim's (on the GPU lattice) write the same text for the test's lattice
+  // (values within 1e-12, printed at the stream's default precision)
+  {
+    Matrix lp(3, 3, std::log(1.0 / 3));
+    const auto lat = ds2ctc::ctc_lattice_gpu(lp, {0}, 2);
+    std::ostringstream mine, theirs;
+    ds2ctc::dump_lattice_tsv(lat, mine);
+    asr::ctc::dump_lattice_tsv(asr::ctc::ctc_lattice(lp, {0}, 2), theirs);
+    check(mine.str().find("# alpha (3 x 3)") != std::string::npos, "tsv alpha header");
+    check(mine.str().find("# beta (3 x 3)") != std::string::npos, "tsv beta header");
+    check(mine.str() == theirs.str(), "tsv text equals the reference's");
+    std::ostringstream conv;  // through the conversion to the reference's lattice type
+    asr::ctc::dump_lattice_tsv(static_cast<asr::ctc::CtcLattice>(lat), conv);
+    check(conv.str() == theirs.str(), "tsv via asr::ctc::CtcLattice");
   }
   // test_ctc.cpp:233-241 -- Viterbi: forced one-to-one alignment
   {

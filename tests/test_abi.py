@@ -158,3 +158,26 @@ def test_fc_backward_entry_points_validate_without_gpu():
     assert L.ds2ctc_fc_backward(p, p, p, p, p, p, 10, 29, 256, p, 16, None) == 1
     # a NULL gradient with any requested output
     assert L.ds2ctc_fc_backward(None, p, p, p, p, p, 10, 29, 256, p, 1 << 20, None) == 1
+
+
+def test_dump_lattice_tsv_format():
+    # dump_lattice_tsv (ctc.cpp:372-383) as test_ctc.cpp:277-284 checks it, on a
+    # hand-made lattice (no GPU): headers, one line per augmented position,
+    # the symbol then tab-separated values in C++ default stream format
+    import io
+
+    import numpy as np
+
+    from paper_1512_02595_b200 import ctc
+
+    a = np.array([[-1.0986122886681098, -2.1972245773362196, -np.inf],
+                  [-1.0986122886681098, -1.504077396776274, -2.1972245773362196],
+                  [-np.inf, -2.1972245773362196, 1e-05]])
+    lat = ctc.CtcLattice([2, 0, 2], a, a * 2, -1.0)
+    buf = io.StringIO()
+    ctc.dump_lattice_tsv(lat, buf)
+    lines = buf.getvalue().splitlines()
+    assert lines[0] == "# alpha (3 x 3)" and lines[4] == "# beta (3 x 3)" and len(lines) == 8
+    assert lines[1] == "2\t-1.09861\t-2.19722\t-inf"
+    assert lines[3] == "2\t-inf\t-2.19722\t1e-05"
+    assert lines[5].split("\t")[0] == "2" and lines[6].split("\t")[0] == "0"
