@@ -1085,38 +1085,65 @@ ds2ctc_status ds2ctc_compute_loss_host(const float* activations, float* gradient
         result = result == DS2CTC_STATUS_SUCCESS ? DS2CTC_STATUS_EXECUTION_FAILED : result;
     return result;
   };
-  for (int c = 0; c < nc; ++c) {
-    cudaStream_t sc = c == 0 ? ctx.stream : ctx.chunk_streams[c - 1];
+  // Two passes over the chunks: every upload and kernel launch first, then
+  // the downloads. The host's enqueue work per chunk (metadata, copies,
+  // launch: ~20-30 us) then stays ahead of the serialised uploads, so the
+  // last chunk's k_pair is not waiting for the host to enqueue the earlier
+  // chunks' downloads (DS2CTC_HOST_TWO_PASS=0: one pass).
+  static const bool two_pass = [] {
+    const char* v = std::getenv("DS2CTC_HOST_TWO_PASS");
+    return v == nullptr || std::atoi(v) != 0;
+  }();
+  auto chunk_stream = [&](int c) { return c == 0 ? ctx.stream : ctx.chunk_streams[c - 1]; };
+  auto chunk_width = [&](int c) { return static_cast<size_t>(b0[c + 1] - b0[c]) * A * sizeof(float); };
+  auto chunk_grads = [&](int c) -> unsigned char* {
+    return !gradients ? nullptr
+           : direct   ? reinterpret_cast<unsigned char*>(g_direct) + x_off[c]
+                      : static_cast<unsigned char*>(ctx.grads) + x_off[c];
+  };
+  auto launch = [&](int c) -> ds2ctc_status {
+    cudaStream_t sc = chunk_stream(c);
     const int bc = b0[c + 1] - b0[c];
-    const size_t w = static_cast<size_t>(bc) * A * sizeof(float);
+    const size_t w = chunk_width(c);
     auto* xd = static_cast<unsigned char*>(ctx.acts) + x_off[c];
     const size_t xpitch = direct ? row : w;
-    auto* gd = !gradients ? nullptr
-               : direct   ? reinterpret_cast<unsigned char*>(g_direct) + x_off[c]
-                          : static_cast<unsigned char*>(ctx.grads) + x_off[c];
     const auto* xh = reinterpret_cast<const unsigned char*>(activations) + static_cast<size_t>(b0[c]) * A * sizeof(float);
     if (serial_upload && c > 0 && cudaStreamWaitEvent(sc, ctx.uploaded[c - 1], 0) != cudaSuccess)
-      return drain(DS2CTC_STATUS_EXECUTION_FAILED);
+      return DS2CTC_STATUS_EXECUTION_FAILED;
     if (t_c[c] > 0 && w > 0 &&
         cudaMemcpy2DAsync(xd, xpitch, xh, row, w, t_c[c], cudaMemcpyHostToDevice, sc) != cudaSuccess)
-      return drain(DS2CTC_STATUS_MEMOPS_FAILED);
+      return DS2CTC_STATUS_MEMOPS_FAILED;
     if (serial_upload && c + 1 < nc && cudaEventRecord(ctx.uploaded[c], sc) != cudaSuccess)
-      return drain(DS2CTC_STATUS_EXECUTION_FAILED);
+      return DS2CTC_STATUS_EXECUTION_FAILED;
     float* cd = static_cast<float*>(ctx.costs) + b0[c];
-    st = run(reinterpret_cast<const float*>(xd), reinterpret_cast<float*>(gd), flat_labels + lab0[c],
-             label_lengths + b0[c], input_lengths + b0[c], A, bc, blank_label, cd,
-             static_cast<unsigned char*>(ctx.ws) + ws_off[c], ws_off[c + 1] - ws_off[c], true, sc, direct ? B : 0);
-    if (st != DS2CTC_STATUS_SUCCESS) return drain(st);
+    return run(reinterpret_cast<const float*>(xd), reinterpret_cast<float*>(chunk_grads(c)), flat_labels + lab0[c],
+               label_lengths + b0[c], input_lengths + b0[c], A, bc, blank_label, cd,
+               static_cast<unsigned char*>(ctx.ws) + ws_off[c], ws_off[c + 1] - ws_off[c], true, sc, direct ? B : 0);
+  };
+  auto download = [&](int c) -> ds2ctc_status {
+    cudaStream_t sc = chunk_stream(c);
+    const int bc = b0[c + 1] - b0[c];
+    const size_t w = chunk_width(c);
     if (gradients && t_c[c] > 0 && w > 0) {
       auto* gh = reinterpret_cast<unsigned char*>(gradients) + static_cast<size_t>(b0[c]) * A * sizeof(float);
-      if (!direct && cudaMemcpy2DAsync(gh, row, gd, w, w, t_c[c], cudaMemcpyDeviceToHost, sc) != cudaSuccess)
-        return drain(DS2CTC_STATUS_MEMOPS_FAILED);
+      if (!direct && cudaMemcpy2DAsync(gh, row, chunk_grads(c), w, w, t_c[c], cudaMemcpyDeviceToHost, sc) != cudaSuccess)
+        return DS2CTC_STATUS_MEMOPS_FAILED;
       // frames past this chunk's longest utterance: zero rows (the contract), on the host
       for (int t = t_c[c]; t < lay.t_max; ++t) std::memset(gh + static_cast<size_t>(t) * row, 0, w);
     }
+    float* cd = static_cast<float*>(ctx.costs) + b0[c];
     if (bc > 0 && cudaMemcpyAsync(costs + b0[c], cd, bc * sizeof(float), cudaMemcpyDeviceToHost, sc) != cudaSuccess)
-      return drain(DS2CTC_STATUS_MEMOPS_FAILED);
+      return DS2CTC_STATUS_MEMOPS_FAILED;
+    return DS2CTC_STATUS_SUCCESS;
+  };
+  for (int c = 0; c < nc; ++c) {
+    st = launch(c);
+    if (st == DS2CTC_STATUS_SUCCESS && !two_pass) st = download(c);
+    if (st != DS2CTC_STATUS_SUCCESS) return drain(st);
   }
+  if (two_pass)
+    for (int c = 0; c < nc; ++c)
+      if ((st = download(c)) != DS2CTC_STATUS_SUCCESS) return drain(st);
   return drain(DS2CTC_STATUS_SUCCESS);
 }
 

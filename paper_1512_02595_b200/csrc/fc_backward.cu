@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <utility>
 #include <cstdint>
+#include <cstdlib>
 
 #include "ds2ctc_internal.h"
 
@@ -181,7 +182,7 @@ __host__ __device__ constexpr int gemm_smem() {
 // STAGES: pipeline depth (1 when K is a single block: several CTAs then share
 // an SM, so one CTA's epilogue stores overlap another's loads).
 template <bool kAMN, bool kBMN, int BN, int STAGES>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, STAGES <= 2 ? 2 : 1)
     k_fc_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, GemmArgs g) {
   constexpr bool kTrans = kAMN || kBMN;
   constexpr int kStages = STAGES;
@@ -496,15 +497,23 @@ int fc_backward(const float* g, const float* x, const float* w, float* dw, float
     // K split: whole waves of the one-CTA-per-SM grid (a partial last wave
     // costs a full one: 20 tiles x 30 splits = 600 CTAs was 4.05 waves),
     // 2-5 waves, the fullest last wave winning (English dW 131 -> 118 us)
+    // Small alphabets: two-stage dW CTAs, two per SM, so one CTA's handoffs
+    // (transpose, MMA, refill) overlap the other's loads: 118 -> 110 us per
+    // English dW (DS2CTC_FC_DW_STAGES=4: one four-stage CTA per SM).
+    static const int dw_stages = [] {
+      const char* v = std::getenv("DS2CTC_FC_DW_STAGES");
+      return v != nullptr && std::atoi(v) == 4 ? 4 : 2;
+    }();
+    const int slots = sm_count * (A <= 32 && dw_stages == 2 ? 2 : 1);  // resident dW CTAs per wave
     auto split_for = [&](int tiles) {
       int best_sp = 1;
       double best_eff = -1.0;
       for (int w = 2; w <= 5; ++w) {
-        const int sp = std::max(1, std::min(kb, w * sm_count / tiles));
+        const int sp = std::max(1, std::min(kb, w * slots / tiles));
         const int kpb = (kb + sp - 1) / sp;
         const int n = (kb + kpb - 1) / kpb;  // splits actually launched
         const long long ctas = static_cast<long long>(n) * tiles;
-        const double eff = static_cast<double>(ctas) / (((ctas + sm_count - 1) / sm_count) * sm_count);
+        const double eff = static_cast<double>(ctas) / (((ctas + slots - 1) / slots) * slots);
         if (eff > best_eff + 1e-9) {
           best_eff = eff;
           best_sp = sp;
@@ -519,7 +528,8 @@ int fc_backward(const float* g, const float* x, const float* w, float* dw, float
         return cudaErrorInvalidValue;
       const auto sp = split_for((H + kTileM - 1) / kTileM);
       GemmArgs ga{H, A, sp.second, rows, dw, H, 1, 1};
-      e = launch_gemm<true, true, 32, 4>(ma, mb, ga, sp.first, s);
+      e = dw_stages == 2 ? launch_gemm<true, true, 32, 2>(ma, mb, ga, sp.first, s)
+                         : launch_gemm<true, true, 32, 4>(ma, mb, ga, sp.first, s);
     } else {
       if (!make_map(&ma, gp, A, rows, ldg, kTileK) || !make_map(&mb, x, H, rows, H, kTileK))
         return cudaErrorInvalidValue;
