@@ -140,10 +140,11 @@ def run(so, A=29, T=700, L=150, B=64, brief=False):
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "variants":
         sets = [tuple(v.split("+")) if v != "base" else () for v in sys.argv[2:]] or [()]
+        shape = [int(v) for v in os.environ.get("SHAPE", "29,700,150,64").split(",")]  # A,T,L,B
         for defs in sets:
             so = build(defs)
-            print("variant", defs or "base")
-            run(so, brief=True)
+            print("variant", defs or "base", "shape", shape)
+            run(so, *shape, brief=True)
     else:
         so = build()
         args = [int(v) for v in sys.argv[1:]]
