@@ -213,9 +213,10 @@ ds2ctc_status ds2ctc_reduce_fault(unsigned long long* seq);
  * every kernel of the pipeline into the next of `slots` event sets (no host
  * synchronisation). ds2ctc_profile_read(i) synchronises on call i (counted
  * from the enable, i < slots) and writes ms[4] = {pair kernel (alpha||beta
- * chain, fused gradient), dense gradient pass (large alphabets: the softmax
- * pass alone, which runs concurrently with the pair kernel), cost
- * finalisation (+ the key-column patch), whole call}. slots == 0 disables.
+ * chain, fused gradient), dense gradient pass (large alphabets: k_dense after
+ * the pair kernel; with DS2CTC_DENSE_OVERLAP=1 the softmax pass alone, which
+ * then runs concurrently with the pair kernel), cost finalisation, whole
+ * call}. slots == 0 disables.
  */
 ds2ctc_status ds2ctc_profile_enable(int slots);
 ds2ctc_status ds2ctc_profile_read(int call_index, float* ms);
