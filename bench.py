@@ -313,8 +313,19 @@ def main():
         gen.manual_seed(4321 + rank)
         fc_x = torch.randn((x.shape[0], B, H), generator=gen, device=dev, dtype=torch.float32)
         fc_w = torch.randn((A, H), generator=gen, device=dev, dtype=torch.float32) * 0.02
-        fc_dw = torch.zeros((A, H), device=dev, dtype=torch.float32)
-        fc_db = torch.zeros(A, device=dev, dtype=torch.float32)
+        # dW and db in one buffer: one parameter-gradient all-reduce per step
+        fc_grad = torch.zeros(A * H + A, device=dev, dtype=torch.float32)
+        fc_dw = fc_grad[:A * H].view(A, H)
+        fc_db = fc_grad[A * H:]
+        vec = None  # f4 over NVLink peer memory (ds2ctc_vec_allreduce); NCCL when unavailable
+        if world > 1 and os.environ.get("DS2CTC_NCCL_REDUCE") != "1":
+            from paper_1512_02595_b200.dist import PeerVecReducer
+
+            vec = PeerVecReducer(A * H + A, dev)
+            if not vec.ok:
+                if rank == 0:
+                    print(f"peer vector all-reduce unavailable ({vec.error}); using NCCL", file=sys.stderr)
+                vec = None
         fc_dx = torch.empty((x.shape[0], B, H), device=dev, dtype=torch.float32)
         fc_ws = ctc.Workspace(dev)
         fc_sz = ctypes.c_size_t()
@@ -329,9 +340,11 @@ def main():
                                           ctypes.c_void_p(fc_db.data_ptr()), ctypes.c_void_p(fc_dx.data_ptr()),
                                           x.shape[0] * B, A, H, ctypes.c_void_p(fc_ws_ptr), fc_ws_bytes,
                                           ctypes.c_void_p(stream.cuda_stream)), "ds2ctc_fc_backward")
-        if world > 1:  # f4: the parameter-gradient all-reduce (trainer.cpp:175, ring_allreduce -> NCCL)
-            dist.all_reduce(fc_dw)
-            dist.all_reduce(fc_db)
+        if world > 1:  # f4: the parameter-gradient all-reduce (trainer.cpp:175, ring_allreduce)
+            if vec is not None:
+                vec.reduce(fc_grad.data_ptr(), stream.cuda_stream)
+            else:
+                dist.all_reduce(fc_grad)
 
     def step(reduce_mode=None):
         st = lib.ds2ctc_compute_loss_checked(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(grads.data_ptr()),
@@ -349,6 +362,18 @@ def main():
         if world > 1:
             dist.all_reduce(pair)
 
+    if H and world > 1 and vec is not None:  # the peer-memory vector all-reduce must agree with NCCL's
+        gen_chk = torch.Generator(device=dev)
+        gen_chk.manual_seed(99 + rank)
+        probe = torch.randn(A * H + A, generator=gen_chk, device=dev, dtype=torch.float32)
+        ref_v = probe.clone()
+        dist.all_reduce(ref_v)
+        fc_grad.copy_(probe)
+        vec.reduce(fc_grad.data_ptr(), stream.cuda_stream)
+        torch.cuda.synchronize()
+        vec.check()
+        if not torch.allclose(fc_grad, ref_v, rtol=1e-5, atol=1e-5):
+            raise RuntimeError("peer vector all-reduce disagrees with NCCL")
     if peer is not None:  # the fused reduction must agree with NCCL's
         step("nccl")
         ref_pair = pair.clone()
@@ -361,7 +386,9 @@ def main():
     # kernels of ours per step: k_pair (+ k_dense + k_finalize for large A) + k_loss_sum / k_loss_allreduce
     if B:
         # large A: k_dense + k_finalize, or (overlapped) k_dense_soft + k_dense_patch + k_finalize
-        launches_per_step = 1 + ((3 if dense_overlap else 2) if A > 128 else 0) + 1 + (5 if H else 0)  # fc: pad, bias, W^T, 2 GEMMs
+        launches_per_step = (1 + ((3 if dense_overlap else 2) if A > 128 else 0) + 1
+                             + (5 if H else 0)  # fc: pad, bias, W^T, 2 GEMMs
+                             + (1 if H and world > 1 and vec is not None else 0))  # f4 peer all-reduce
     else:
         launches_per_step = 1
 
@@ -433,6 +460,8 @@ def main():
     torch.cuda.synchronize()
     if peer is not None:
         peer.check()
+    if H and vec is not None:
+        vec.check()
     if world > 1:
         dist.barrier()
     clocks = sampler.stop() if sampler else None
@@ -587,7 +616,9 @@ def main():
                                    "frac_hbm": fc_bytes / (fc_ms / 1e3) / 1e9 / peak if fc_ms else None,
                                    "tflops": fc_flops / (fc_ms / 1e3) / 1e12 if fc_ms else None,
                                    "kernels": "tcgen05 kind::tf32 (k_fc_gemm x2) + bias sum + W^T + row pad",
-                                   "param_grad_allreduce": "nccl all_reduce (dW, db)" if world > 1 else "none"}
+                                   "param_grad_allreduce": ("nvlink peer memory (ds2ctc_vec_allreduce, dW + db)"
+                                                            if world > 1 and vec is not None else
+                                                            "nccl all_reduce (dW + db)" if world > 1 else "none")}
         if world == 1 and not args.no_cpu_baseline:
             # The reference CPU CTC on the same inputs: (i) all host cores, one
             # utterance per thread (the paper's CPU CTC); (ii) one

@@ -198,6 +198,24 @@ ds2ctc_status ds2ctc_mailbox_close(void* peer_mailbox, int own);
 ds2ctc_status ds2ctc_loss_sum_allreduce(const float* costs, int minibatch, double* out2, void* const* peer_mailboxes,
                                         int rank, int world, unsigned long long seq, void* stream);
 /*
+ * Parameter-gradient all-reduce over NVLink peer memory (trainer.cpp:175:
+ * ring_allreduce of the gradients, allreduce.cpp:301-341): every rank's
+ * data[n] (fp32, device) becomes the sum over ranks folded in rank order
+ * (allreduce.hpp:91-95) -- bitwise identical on every rank and run to run.
+ * Setup once per rank: ds2ctc_exchange_size(n) bytes from
+ * ds2ctc_exchange_alloc (zeroed; 64-byte CUDA IPC handle out), the peers'
+ * regions mapped with ds2ctc_mailbox_open, released with ds2ctc_mailbox_close.
+ * Every rank calls with the same n, its rank, world (<= 8) and the same seq
+ * (1, 2, 3, ... per call). One kernel: each CTA stages its slice, publishes
+ * a per-slice flag to every rank, waits for every rank's flag (at most 20 s;
+ * on timeout the slice is NaN and ds2ctc_reduce_fault reports seq), folds.
+ */
+ds2ctc_status ds2ctc_exchange_size(size_t n, size_t* bytes);
+ds2ctc_status ds2ctc_exchange_alloc(size_t bytes, void** region, void* ipc_handle);
+ds2ctc_status ds2ctc_vec_allreduce(float* data, size_t n, void* const* peer_regions, int rank, int world,
+                                   unsigned long long seq, void* stream);
+
+/*
  * Lost-peer check of ds2ctc_loss_sum_allreduce. Each call waits at most 20 s
  * (%globaltimer) for the peers' pairs of its step; on timeout it writes NaN
  * into out2 (never a stale fold) and records the step. This reads (after

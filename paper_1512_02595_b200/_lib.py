@@ -35,6 +35,9 @@ EXPORTS = (
     "ds2ctc_mailbox_open",
     "ds2ctc_mailbox_close",
     "ds2ctc_loss_sum_allreduce",
+    "ds2ctc_exchange_size",
+    "ds2ctc_exchange_alloc",
+    "ds2ctc_vec_allreduce",
     "ds2ctc_reduce_fault",
     "ds2ctc_fc_backward_workspace_size",
     "ds2ctc_fc_backward",
@@ -127,6 +130,13 @@ def lib():
             L.ds2ctc_fc_backward.restype = ctypes.c_int
             L.ds2ctc_fc_backward.argtypes = [_p, _p, _p, _p, _p, _p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p,
                                              ctypes.c_size_t, _p]
+            L.ds2ctc_exchange_size.restype = ctypes.c_int
+            L.ds2ctc_exchange_size.argtypes = [ctypes.c_size_t, _szp]
+            L.ds2ctc_exchange_alloc.restype = ctypes.c_int
+            L.ds2ctc_exchange_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p), _p]
+            L.ds2ctc_vec_allreduce.restype = ctypes.c_int
+            L.ds2ctc_vec_allreduce.argtypes = [_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int,
+                                               ctypes.c_int, ctypes.c_ulonglong, _p]
             L.ds2ctc_reduce_fault.restype = ctypes.c_int
             L.ds2ctc_reduce_fault.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
             L.ds2ctc_viterbi_get_workspace_size.restype = ctypes.c_int

@@ -906,6 +906,40 @@ ds2ctc_status ds2ctc_mailbox_close(void* peer_mailbox, int own) {
   return e == cudaSuccess ? DS2CTC_STATUS_SUCCESS : DS2CTC_STATUS_EXECUTION_FAILED;
 }
 
+ds2ctc_status ds2ctc_exchange_size(size_t n, size_t* bytes) {
+  if (bytes == nullptr) return DS2CTC_STATUS_INVALID_VALUE;
+  *bytes = vec_exchange_bytes(static_cast<long long>(n));
+  return DS2CTC_STATUS_SUCCESS;
+}
+
+ds2ctc_status ds2ctc_exchange_alloc(size_t bytes, void** region, void* ipc_handle) {
+  if (region == nullptr || ipc_handle == nullptr || bytes == 0) return DS2CTC_STATUS_INVALID_VALUE;
+  if (cudaMalloc(region, bytes) != cudaSuccess) return DS2CTC_STATUS_MEMOPS_FAILED;
+  if (cudaMemset(*region, 0, bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+    return DS2CTC_STATUS_MEMOPS_FAILED;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, *region) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
+  std::memcpy(ipc_handle, &h, sizeof(h));
+  return DS2CTC_STATUS_SUCCESS;
+}
+
+ds2ctc_status ds2ctc_vec_allreduce(float* data, size_t n, void* const* peer_regions, int rank, int world,
+                                   unsigned long long seq, void* stream) {
+  if ((n > 0 && data == nullptr) || peer_regions == nullptr || world < 1 || world > kMaxPeers || rank < 0 ||
+      rank >= world || seq == 0)
+    return DS2CTC_STATUS_INVALID_VALUE;
+  PeerMailboxes pr{};
+  for (int r = 0; r < world; ++r) {
+    if (peer_regions[r] == nullptr) return DS2CTC_STATUS_INVALID_VALUE;
+    pr.peer[r] = peer_regions[r];
+  }
+  pr.rank = rank;
+  pr.world = world;
+  if (launch_vec_allreduce(data, static_cast<long long>(n), pr, seq, stream) != cudaSuccess)
+    return DS2CTC_STATUS_EXECUTION_FAILED;
+  return DS2CTC_STATUS_SUCCESS;
+}
+
 ds2ctc_status ds2ctc_loss_sum_allreduce(const float* costs, int minibatch, double* out2, void* const* peer_mailboxes,
                                         int rank, int world, unsigned long long seq, void* stream) {
   if (out2 == nullptr || minibatch < 0 || (minibatch > 0 && costs == nullptr) || peer_mailboxes == nullptr ||

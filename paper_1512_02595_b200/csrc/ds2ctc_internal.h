@@ -314,6 +314,8 @@ struct PeerMailboxes {
 int launch_loss_allreduce(const float* costs, int B, double* out2, const PeerMailboxes& mb, unsigned long long seq,
                           void* stream);
 size_t mailbox_bytes(int world);
+size_t vec_exchange_bytes(long long n);
+int launch_vec_allreduce(float* data, long long n, const PeerMailboxes& pr, unsigned long long seq, void* stream);
 int read_reduce_fault(unsigned long long* seq);
 int read_watchdog(unsigned long long* out4);
 size_t viterbi_smem_bytes(int T, int L);

@@ -151,3 +151,90 @@ class PeerLossReducer:
             self.lib.ds2ctc_mailbox_close(ctypes.c_void_p(self.own), 1)
         self.opened = []
         self.own = None
+
+
+class PeerVecReducer:
+    """The parameter-gradient all-reduce of trainer.cpp:175 (ring_allreduce,
+    allreduce.cpp:301-341) over NVLink peer memory (ds2ctc_vec_allreduce): one
+    kernel per call, rank-ordered fold (bitwise identical on every rank), no
+    NCCL call on the step. One exchange region per rank for vectors of `n`
+    floats; setup exchanges CUDA IPC handles once over the default process
+    group, and `ok` is the group's agreement (all ranks succeeded)."""
+
+    def __init__(self, n: int, device):
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+
+        self.lib = _lib.lib()
+        self.n = int(n)
+        self.rank = dist.get_rank()
+        self.world = dist.get_world_size()
+        self.opened = []
+        self.own = None
+        self.seq = 0
+        err = None
+        own = ctypes.c_void_p()
+        handle = (ctypes.c_char * 64)()
+        size = ctypes.c_size_t()
+        if self.world > 8:
+            err = "more than 8 ranks"
+        elif self.lib.ds2ctc_exchange_size(self.n, ctypes.byref(size)) != 0 or \
+                self.lib.ds2ctc_exchange_alloc(size.value, ctypes.byref(own), handle) != 0:
+            err = "exchange alloc / IPC handle failed"
+        else:
+            self.own = own.value
+        handles = [None] * self.world
+        dist.all_gather_object(handles, None if err else bytes(handle))
+        self.ptrs = (ctypes.c_void_p * max(self.world, 1))()
+        if err is None:
+            for r in range(self.world):
+                if r == self.rank:
+                    self.ptrs[r] = self.own
+                    continue
+                if handles[r] is None:
+                    err = f"rank {r} has no exchange region"
+                    break
+                p = ctypes.c_void_p()
+                h = (ctypes.c_char * 64).from_buffer_copy(handles[r])
+                if self.lib.ds2ctc_mailbox_open(h, ctypes.byref(p)) != 0:
+                    err = f"IPC open of rank {r}'s exchange region failed"
+                    break
+                self.ptrs[r] = p.value
+                self.opened.append(p.value)
+        flag = torch.tensor([0 if err else 1], dtype=torch.int32, device=device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        self.ok = bool(flag.item())
+        self.error = err
+        if not self.ok:
+            self.close()
+
+    def reduce(self, data_ptr: int, stream_ptr: int) -> None:
+        """In place: data[n] (fp32, device) <- sum over ranks in rank order."""
+        from . import _lib
+
+        if self.own is None:
+            raise RuntimeError("PeerVecReducer is closed (a peer was lost); rebuild it on every rank")
+        self.seq += 1
+        _lib.check(self.lib.ds2ctc_vec_allreduce(ctypes.c_void_p(data_ptr), self.n,
+                                                 ctypes.cast(self.ptrs, ctypes.POINTER(ctypes.c_void_p)),
+                                                 self.rank, self.world, self.seq, ctypes.c_void_p(stream_ptr)),
+                   "ds2ctc_vec_allreduce")
+
+    def check(self) -> None:
+        """Raises (and closes) if a peer wait of any peer-memory collective timed out."""
+        from . import _lib
+
+        seq = _lib.reduce_fault()
+        if seq is not None:
+            self.close()
+            raise RuntimeError(f"peer-memory all-reduce: peer wait timed out at step {seq}")
+
+    def close(self) -> None:
+        for p in self.opened:
+            self.lib.ds2ctc_mailbox_close(ctypes.c_void_p(p), 0)
+        self.opened = []
+        if self.own is not None:
+            self.lib.ds2ctc_mailbox_close(ctypes.c_void_p(self.own), 1)
+            self.own = None

@@ -96,6 +96,34 @@ def main():
             dist.barrier()
         else:
             peer.close()
+            # f4: the parameter-gradient all-reduce over peer memory (ds2ctc_vec_allreduce),
+            # an odd length (the dW + db buffer of the English output layer: 29 x 2560 + 29)
+            from paper_1512_02595_b200.dist import PeerVecReducer
+
+            n = 29 * 2560 + 29
+            vec = PeerVecReducer(n, dev)
+            assert vec.ok, vec.error
+            gen = torch.Generator(device=dev)
+            sums, nccl_sums, folds = [], [], []
+            for step in range(3):  # the two exchange banks alternate
+                gen.manual_seed(1000 * step + rank)
+                v = torch.randn(n, generator=gen, device=dev, dtype=torch.float32)
+                mine = v.clone()
+                vec.reduce(mine.data_ptr(), stream)
+                ref = v.clone()
+                dist.all_reduce(ref)
+                parts = [torch.empty_like(v) for _ in range(world)]
+                dist.all_gather(parts, v)
+                fold = torch.zeros_like(v)
+                for part in parts:  # rank order, fp32 left to right: the kernel's fold
+                    fold += part
+                torch.cuda.synchronize()
+                sums.append(float(mine.double().sum()))
+                nccl_sums.append(float((mine - ref).abs().max()))
+                folds.append(bool(torch.equal(mine, fold)))
+            vec.check()
+            vec.close()
+            out.update(vec_sum=sums, vec_vs_nccl=nccl_sums, vec_fold_bitwise=folds)
         if rank == 0:
             import oracle  # the checker (test infrastructure)
 

@@ -64,6 +64,18 @@ def test_two_gpu_scalar_reduce_matches_nccl_and_oracle(tmp_path):
 
 
 @pytest.mark.skipif(_gpus() < 2, reason="needs 2 GPUs")
+def test_two_gpu_parameter_gradient_allreduce(tmp_path):
+    # f4 (trainer.cpp:175): ds2ctc_vec_allreduce over NVLink peer memory equals
+    # the rank-ordered fp32 fold bitwise on both ranks, and NCCL's all-reduce
+    # within fp32 rounding
+    r0, r1 = _run(tmp_path)
+    for r in (r0, r1):
+        assert all(r["vec_fold_bitwise"]), r["vec_fold_bitwise"]
+        assert max(r["vec_vs_nccl"]) <= 1e-5, r["vec_vs_nccl"]
+    assert r0["vec_sum"] == r1["vec_sum"], "every rank must fold to the bitwise-same vector"
+
+
+@pytest.mark.skipif(_gpus() < 2, reason="needs 2 GPUs")
 def test_two_gpu_lost_peer_reports_fault(tmp_path):
     r0, r1 = _run(tmp_path, "--lost-peer")
     assert r0["fault"] is not None and "timed out" in r0["fault"], r0
