@@ -630,6 +630,25 @@ bool grow(void** p, size_t* cap, size_t want) {
   return true;
 }
 
+// Zeroed device memory for a peer-memory collective and its CUDA IPC handle;
+// freed again on any failure after the allocation.
+ds2ctc_status ipc_region_alloc(size_t bytes, void** region, void* ipc_handle) {
+  if (cudaMalloc(region, bytes) != cudaSuccess) return DS2CTC_STATUS_MEMOPS_FAILED;
+  cudaIpcMemHandle_t h;
+  ds2ctc_status st = DS2CTC_STATUS_SUCCESS;
+  if (cudaMemset(*region, 0, bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+    st = DS2CTC_STATUS_MEMOPS_FAILED;
+  else if (cudaIpcGetMemHandle(&h, *region) != cudaSuccess)
+    st = DS2CTC_STATUS_EXECUTION_FAILED;
+  if (st != DS2CTC_STATUS_SUCCESS) {
+    cudaFree(*region);
+    *region = nullptr;
+    return st;
+  }
+  std::memcpy(ipc_handle, &h, sizeof(h));
+  return DS2CTC_STATUS_SUCCESS;
+}
+
 }  // namespace
 }  // namespace ds2ctc
 
@@ -881,14 +900,7 @@ ds2ctc_status ds2ctc_ctc_lattice(const float* activations, const int* flat_label
 
 ds2ctc_status ds2ctc_mailbox_alloc(int world, void** mailbox, void* ipc_handle) {
   if (mailbox == nullptr || ipc_handle == nullptr || world < 1 || world > kMaxPeers) return DS2CTC_STATUS_INVALID_VALUE;
-  const size_t bytes = mailbox_bytes(world);
-  if (cudaMalloc(mailbox, bytes) != cudaSuccess) return DS2CTC_STATUS_MEMOPS_FAILED;
-  if (cudaMemset(*mailbox, 0, bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
-    return DS2CTC_STATUS_MEMOPS_FAILED;
-  cudaIpcMemHandle_t h;
-  if (cudaIpcGetMemHandle(&h, *mailbox) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
-  std::memcpy(ipc_handle, &h, sizeof(h));
-  return DS2CTC_STATUS_SUCCESS;
+  return ipc_region_alloc(mailbox_bytes(world), mailbox, ipc_handle);
 }
 
 ds2ctc_status ds2ctc_mailbox_open(const void* ipc_handle, void** peer_mailbox) {
@@ -914,13 +926,7 @@ ds2ctc_status ds2ctc_exchange_size(size_t n, size_t* bytes) {
 
 ds2ctc_status ds2ctc_exchange_alloc(size_t bytes, void** region, void* ipc_handle) {
   if (region == nullptr || ipc_handle == nullptr || bytes == 0) return DS2CTC_STATUS_INVALID_VALUE;
-  if (cudaMalloc(region, bytes) != cudaSuccess) return DS2CTC_STATUS_MEMOPS_FAILED;
-  if (cudaMemset(*region, 0, bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
-    return DS2CTC_STATUS_MEMOPS_FAILED;
-  cudaIpcMemHandle_t h;
-  if (cudaIpcGetMemHandle(&h, *region) != cudaSuccess) return DS2CTC_STATUS_EXECUTION_FAILED;
-  std::memcpy(ipc_handle, &h, sizeof(h));
-  return DS2CTC_STATUS_SUCCESS;
+  return ipc_region_alloc(bytes, region, ipc_handle);
 }
 
 ds2ctc_status ds2ctc_vec_allreduce(float* data, size_t n, void* const* peer_regions, int rank, int world,
