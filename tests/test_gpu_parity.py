@@ -354,6 +354,33 @@ def test_fused_loss_allreduce_single_rank(cuda):
     assert lib.ds2ctc_mailbox_close(own, 1) == 0
 
 
+@pytest.mark.parametrize("case", range(24))
+def test_random_shapes_vs_oracle(cuda, case):
+    # A seeded sweep over the shape space the ABI accepts: small and large
+    # alphabets (fused / split path), ragged T (including T = 0 and 1), label
+    # lengths up to and past feasibility, repeats, any blank, logit scales from
+    # flat to peaked -- each batch against the fp64 oracle element by element
+    rng = np.random.default_rng(5000 + case)
+    A = int(rng.choice([2, 3, 5, 29, 64, 128, 129, 300]))
+    B = int(rng.integers(1, 24))
+    T = rng.integers(0, 260, size=B).astype(np.int32)
+    L = np.array([rng.integers(0, max(1, t // 2 + 3)) for t in T], dtype=np.int32)
+    scale = float(rng.choice([0.5, 1.0, 4.0, 8.0]))
+    acts, flat, ll, il = make_batch(A, T, L, seed=9000 + case, scale=scale)
+    blank = int(rng.integers(0, A))
+    # labels drawn from the symbols other than the blank, with runs of repeats
+    flat = np.where(flat >= blank, flat + 1, flat).astype(np.int32) % A
+    flat = np.where(flat == blank, (blank + 1) % A, flat).astype(np.int32)
+    if flat.size > 4:
+        runs = rng.integers(0, flat.size - 1, size=max(1, flat.size // 8))
+        flat[runs + 1] = flat[runs]
+    if acts.shape[0] == 0:
+        return
+    costs, grads = run_gpu(acts, flat, ll, il, blank=blank)
+    rc, rg = oracle.oracle_batch(acts, flat, ll, il, blank=blank, nthreads=8)
+    assert_parity(costs, grads, rc, rg, il, f"random{case}-A{A}")
+
+
 # The parity margin the round-2 verdict asks for: every config above at most
 # 2e-5 absolute on the gradient (5x inside the 1e-4 contract). Runs last.
 GRAD_MARGIN = 2.5e-5
@@ -366,3 +393,4 @@ def test_zz_gradient_margin_summary(cuda):
     for k, (rc, ge) in sorted(ERRORS.items()):
         print(f"MARGIN {k}: rel cost {rc:.2e}, abs grad {ge:.2e}")
     assert worst[1][1] <= GRAD_MARGIN, f"gradient margin: {worst[0]} at {worst[1][1]:.3e} > {GRAD_MARGIN}"
+
